@@ -1,0 +1,190 @@
+/*
+ * cog_b200.h -- C-ABI of the B200-native Cascade-of-Gaussians hot path.
+ *
+ * Plain pointers and sizes; every pointer is a DEVICE pointer unless stated
+ * otherwise; every call is asynchronous on `stream` (a cudaStream_t passed
+ * as void*).  Return value: 0 on success, a positive cudaError_t from the
+ * launch, or a negative COG_E* code for rejected arguments (nothing is
+ * launched then).  The caller owns every buffer; nothing is allocated here.
+ *
+ * Each entry point replaces one reference interface of the `cogbg`
+ * package (paths under /root/reference/pkg/src/cogbg/):
+ *
+ *   cog_prior_build      scene_prior.build_kde              :92-112
+ *                        scene_prior.compute_residue_histogram :171-189
+ *                        scene_prior.classify_pixel_dynamics :192-202
+ *                        cascade.CascadeEngine._finalize_tables :213-216
+ *   cog_gmm_warmup       training.train_engine GMM loop      :38-52
+ *                        gmm.init_plane                      gmm.py:89-100
+ *                        grouping.behavior_features           grouping.py:85-91
+ *                        cascade.CascadeEngine._seed_level_order (mode refs) :218-235
+ *   cog_set_levels       cascade.CascadeEngine._seed_level_order (level order) :236-241
+ *   cog_step             kernels_numba.cascade_frame          :152-360
+ *                        kernels_numba.resolve_copies         :363-373
+ *                        cascade.CascadeEngine.process_frame  :261-318
+ *                        cascade.CascadeEngine._update_groups :320-344
+ *                        cascade.CascadeEngine._collect_stats :346-359
+ *   cog_finalize         the per-frame tail of process_frame  :303-317
+ *                        (group update, stats, illumination test) for
+ *                        row-band shards after the partials are summed
+ *   cog_apply_pending    cascade.CascadeEngine._reset_on_illumination :361-391
+ *                        cascade.CascadeEngine.reorder_levels :393-417
+ *   cog_baseline_frame   gmm.classify_frame                   gmm.py:112-133
+ *                        (kernels_numba.baseline_frame :137-149)
+ *   cog_export_state /   the engine's numpy state views, in the reference
+ *   cog_import_state     dtypes and layouts (cascade.py:143-158), used by
+ *                        model_io.save_model / load_model (model_io.py:61-227)
+ *
+ * State layout in HBM (one stream; `streams` copies back to back):
+ *   mixture  mu, var, w : T[depth][k][P]      T = float or double
+ *   meta     u16[depth][P]   count | mid_order | mode_ref (packed)
+ *   dyn      u32[depth][P]   chp_prev | last_label | waking | last_active | clock
+ *   streak   u32[depth][P]
+ *   hits     u32[depth][5][P]
+ *   table    f32[depth][P][256], peak f32[depth][P]
+ *   cls      u8[P], gid u16[P] (0xFFFF = ungrouped)
+ *   g_mu, g_var  f64[depth][G], g_members u32[G]
+ *   accum    u64[cog_accum_words()], sync u32[4]
+ */
+#ifndef COG_B200_H
+#define COG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COG_OK 0
+#define COG_EINVAL (-1)
+#define COG_EUNSUPPORTED (-2)
+
+typedef struct cog_geom {
+  int64_t total_pixels; /* pixels of the FULL frame (illumination threshold) */
+  int32_t height;       /* rows held by this engine (a row band or a frame) */
+  int32_t width;
+  int32_t depth;        /* planes, 1..4 */
+  int32_t k;            /* k_max, 1..8 */
+  int32_t stride;       /* sampling lattice stride, 1..32 */
+  int32_t n_groups;     /* G (groups per stream, max over streams) */
+  int32_t streams;      /* independent streams stored back to back */
+  int32_t state_f64;    /* 0: float32 mixture storage, 1: float64 */
+  int32_t row0;         /* global row of this band's first row (% stride == 0) */
+  int32_t pad_;
+} cog_geom;
+
+typedef struct cog_params {
+  double learning_rate, match_lambda, background_threshold, variance_floor;
+  double initial_variance, chp_epsilon, confidence_threshold, prior_floor;
+  double rate_floor, illumination_fraction;
+  double weights[9]; /* dynamics class c -> (alpha, beta, gamma) at [3c..3c+2] */
+  int32_t saturation_frames, sleep_frames;
+  int32_t sampling_on, grouping_on, rate_scaling_on, chp_on;
+  int32_t literal_conf, compat;
+  int32_t exact_group_sums; /* parity/debug: sum group confidences in the
+                               reference's sequential pixel order (one
+                               thread per group; small frames only) */
+  int32_t pad_;
+} cog_params;
+
+typedef struct cog_state {
+  void *mu, *var, *w;
+  uint16_t *meta;
+  uint32_t *dyn;
+  uint32_t *streak;
+  uint32_t *hits;
+  const float *table;
+  const float *peak;
+  const uint8_t *cls;
+  const uint16_t *gid;
+  double *g_mu, *g_var;
+  const uint32_t *g_members;
+  uint64_t *accum;
+  uint32_t *sync;
+} cog_state;
+
+/* Words of `accum` per stream (kinds, foreground, group partials). */
+int64_t cog_accum_words(int32_t depth, int32_t n_groups);
+
+/* Scene prior for one stream: frames u8[N][depth][P].  Writes, for each
+ * trailing window windows[j] (ascending, last == N), tables
+ * f32[n_windows][depth][P][256]; peak f32[depth][P] of the last window
+ * (<= 0 -> 1); optional hist u16[depth][P][256] (last window counts);
+ * residue u32[P][3] (optional) and the dynamics class u8[P].
+ * kern: f64[256][256] smoothing matrix (scene_prior._kernel_matrix). */
+int cog_prior_build(const uint8_t *frames, int32_t n_frames, int32_t depth,
+                    int64_t n_pix, const double *kern, const int32_t *windows,
+                    int32_t n_windows, float *tables, float *peak,
+                    uint16_t *hist, double residue_t1, double residue_t2,
+                    double peaky_threshold, uint32_t *residue, uint8_t *cls,
+                    void *stream);
+
+/* GMM warm-up over N training frames u8[N][depth][P] for one stream.
+ * Writes the mixture (state dtype per geom.state_f64), meta (count + mode
+ * references ranked by prior mass, ties by w/sigma; mid_order left as
+ * "ungrouped"), dyn (chp_prev = last frame), zeroes streak and hits.
+ * Optional: features f64[P][2] (temporal variance of channel-0 rank-0
+ * variance / weight series) and w_final f64[P]. */
+int cog_gmm_warmup(const cog_geom *geom, const cog_params *prm,
+                   const cog_state *st, const uint8_t *frames,
+                   int32_t n_frames, double *features, double *w_final,
+                   void *stream);
+
+/* Level order seeding from the group map (grouped -> GROUP,MEAN,MEANVAR). */
+int cog_set_levels(const cog_geom *geom, const cog_state *st, void *stream);
+
+/* One frame for all streams: frame u8[streams][depth][P].  Outputs mask
+ * u8[streams][P] (0/255), conf T[streams][depth][P], kind u8[streams]
+ * [depth][P] and stats i64[streams][16] = {frame, n_chp, n_group, n_mean,
+ * n_meanvar, n_gmm, n_skipped, n_foreground, unexplained, fired, ...}.
+ * reorder_now: apply the scheduled level reorder before this frame.
+ * fuse_finalize: 1 = the last CTA of each stream finalizes the frame
+ * (single engine); 0 = leave the summed partials in accum for an external
+ * all-reduce followed by cog_finalize (row-band shards). */
+int cog_step(const cog_geom *geom, const cog_params *prm, const cog_state *st,
+             const uint8_t *frame, uint8_t *mask, void *conf, uint8_t *kind,
+             int64_t *stats, int64_t frame_index, int32_t reorder_now,
+             int32_t fuse_finalize, void *stream);
+
+int cog_finalize(const cog_geom *geom, const cog_params *prm,
+                 const cog_state *st, int64_t *stats, int64_t frame_index,
+                 void *stream);
+
+/* Materialise a pending illumination reset (device flag) and/or a level
+ * reorder (reorder_now) so the state reads as the reference's would. */
+int cog_apply_pending(const cog_geom *geom, const cog_params *prm,
+                      const cog_state *st, int32_t reorder_now, void *stream);
+
+/* Plain per-pixel mixture over all planes of one frame (baseline model):
+ * state uses st->mu/var/w/meta (count only); mask u8[P] 0/255. */
+int cog_baseline_frame(const cog_geom *geom, const cog_params *prm,
+                       const cog_state *st, const uint8_t *frame,
+                       uint8_t *mask, void *stream);
+
+/* Reference-layout views of one stream's state (device buffers):
+ * mu/var/w f64[d][P][K]; count i64[d][P]; mid i8[d][P][3]; ref i8[d][P][2];
+ * chp u8[d][P]; label u8[d][P]; active i8[d][P]; waking u8[d][P];
+ * streak i64[d][P]; clock i64[d][P]; hits i64[d][P][5]. */
+typedef struct cog_ref_state {
+  double *mu, *var, *w;
+  int64_t *count;
+  int8_t *mid, *ref;
+  uint8_t *chp, *label;
+  int8_t *active;
+  uint8_t *waking;
+  int64_t *streak, *clock, *hits;
+} cog_ref_state;
+
+int cog_export_state(const cog_geom *geom, const cog_state *st,
+                     const cog_ref_state *out, void *stream);
+int cog_import_state(const cog_geom *geom, const cog_state *st,
+                     const cog_ref_state *in, void *stream);
+
+/* Version / build string (host pointer, static). */
+const char *cog_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COG_B200_H */

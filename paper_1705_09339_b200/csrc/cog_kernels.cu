@@ -1,0 +1,1401 @@
+// cog_kernels.cu -- B200 (sm_100a) kernels of the Cascade-of-Gaussians hot
+// path and the C-ABI declared in include/cog_b200.h.
+//
+// Kernels (one launch each, all asynchronous on the caller's stream):
+//   prior_kernel     training prior: one CTA stages 32 pixels x N frames of
+//                    one stream in shared memory, builds per-pixel 256-bin
+//                    histograms for each trailing window (bin-major,
+//                    conflict-free, no atomics), smooths them with the
+//                    grid-normalised Gaussian over the distinct sample
+//                    values only, and writes the f32 tables, the peak, the
+//                    pooled residue counts and the dynamics class.
+//   warmup_kernel    GMM warm-up: one thread per plane-pixel streams the N
+//                    training frames with the mixture in registers
+//                    (binary64), records the channel-0 adaptation
+//                    statistics for grouping and seeds the mode references.
+//   step_kernel      the fused per-frame step: persistent CTAs sweep
+//                    stride-aligned warp tiles (stride rows x cw columns),
+//                    run skip/copy gating, confidence, cascade descent and
+//                    bookkeeping per plane-pixel, resolve copies from the
+//                    tile's shared-memory labels, write the union mask, and
+//                    reduce level counts + per-group partials (exact
+//                    integer/fixed-point sums, so the result is independent
+//                    of CTA count and order).  The last CTA of each stream
+//                    applies the group update, the illumination test and the
+//                    frame statistics.  A pending illumination reset or a
+//                    scheduled reorder is applied lazily per pixel at the
+//                    start of the next frame (they touch disjoint state).
+//   finalize_kernel  the same tail for row-band shards after an all-reduce.
+//   pending_kernel   materialises a pending reset / reorder on demand.
+//   baseline_kernel  plain mixture over all planes (gmm.classify_frame).
+//   export/import    reference-layout (f64 / i64) views of the packed state.
+#include "cog_device.cuh"
+#include "../../include/cog_b200.h"
+
+#include <cstdio>
+
+using namespace cog;
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int STEP_THREADS = 256;
+constexpr int PRIOR_PIX = 32;
+constexpr int STATS_WORDS = 16;
+
+// accumulator layout (u64 words, per stream)
+__host__ __device__ inline int acc_kind(int c, int k) { return c * 7 + k; }
+__host__ __device__ inline int acc_fg(int d) { return 7 * d; }
+__host__ __device__ inline int acc_grp(int d, int G, int c, int g) {
+  return 7 * d + 1 + (c * G + g) * 6;
+}
+__host__ __device__ inline int acc_words(int d, int G) {
+  return 7 * d + 1 + 6 * d * G;
+}
+// per (c, g): 0 hit count, 1 sum v over hits, 2 conf hi, 3 conf lo,
+//             4 sum v over all members, 5 member count
+constexpr int CONF_SPLIT = 26;  // conf fixed point: q = floor(conf * 2^52)
+
+struct StepArgs {
+  cog_geom g;
+  cog_params q;
+  cog_state s;
+  const uint8_t* frame;
+  uint8_t* mask;
+  void* conf;
+  uint8_t* kind;
+  int64_t* stats;
+  int64_t frame_index;
+  int reorder_now;
+  int fuse_finalize;
+  int cw, iters, tiles_x, n_tiles;
+};
+
+template <typename T>
+struct MixPtrs {
+  T* mu;
+  T* var;
+  T* w;
+};
+
+// ---------------------------------------------------------------------------
+// mixture load / store (k-th mode of a plane-pixel lives at k*P + p)
+// ---------------------------------------------------------------------------
+template <typename T, int KMAX>
+__device__ __forceinline__ void load_mix(const MixPtrs<T>& m, size_t P,
+                                         size_t p, int n, Mix<KMAX>& x) {
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    x.mu[k] = 0.0;
+    x.var[k] = 1.0;
+    x.w[k] = 0.0;
+    if (k < n) {
+      x.mu[k] = ldrw(m.mu + k * P + p);
+      x.var[k] = ldrw(m.var + k * P + p);
+      x.w[k] = ldrw(m.w + k * P + p);
+    }
+  }
+}
+
+template <typename T, int KMAX>
+__device__ __forceinline__ void store_mix(const MixPtrs<T>& m, size_t P,
+                                          size_t p, int n, const Mix<KMAX>& x) {
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k < n) {
+      st(m.mu + k * P + p, x.mu[k]);
+      st(m.var + k * P + p, x.var[k]);
+      st(m.w + k * P + p, x.w[k]);
+    }
+  }
+}
+
+__device__ __forceinline__ double clip_rint(double x) {
+  double r = rint(x);
+  return r < 0.0 ? 0.0 : (r > 255.0 ? 255.0 : r);
+}
+
+// ---------------------------------------------------------------------------
+// One plane of one stream, by value (cold-path functions take it in
+// registers; no pointer-to-struct round trips through local memory).
+// ---------------------------------------------------------------------------
+template <typename T>
+struct PlaneRef {
+  T* mu;
+  T* var;
+  T* w;
+  uint16_t* meta;
+  uint32_t* dyn;
+  uint32_t* streak;
+  uint32_t* hits;
+  const float* table;
+  const float* peak;
+  size_t P;
+};
+
+template <typename T>
+__device__ __forceinline__ PlaneRef<T> plane_ref(const StepArgs& a, int s,
+                                                 int c) {
+  const size_t P = (size_t)a.g.height * a.g.width;
+  const size_t sc = (size_t)s * a.g.depth + c;
+  const size_t K = (size_t)a.g.k;
+  PlaneRef<T> r;
+  r.mu = (T*)a.s.mu + sc * K * P;
+  r.var = (T*)a.s.var + sc * K * P;
+  r.w = (T*)a.s.w + sc * K * P;
+  r.meta = a.s.meta + sc * P;
+  r.dyn = a.s.dyn + sc * P;
+  r.streak = a.s.streak + sc * P;
+  r.hits = a.s.hits + sc * 5 * P;
+  r.table = a.s.table + sc * P * 256;
+  r.peak = a.s.peak + sc * P;
+  r.P = P;
+  return r;
+}
+
+template <typename T, int KMAX>
+__device__ __forceinline__ void load_mix_r(const PlaneRef<T>& r, size_t p,
+                                           int n, Mix<KMAX>& x) {
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    x.mu[k] = 0.0;
+    x.var[k] = 1.0;
+    x.w[k] = 0.0;
+    if (k < n) {
+      x.mu[k] = ldrw(r.mu + k * r.P + p);
+      x.var[k] = ldrw(r.var + k * r.P + p);
+      x.w[k] = ldrw(r.w + k * r.P + p);
+    }
+  }
+}
+
+template <typename T, int KMAX>
+__device__ __forceinline__ void store_mix_r(const PlaneRef<T>& r, size_t p,
+                                            int n, const Mix<KMAX>& x) {
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k < n) {
+      st(r.mu + k * r.P + p, x.mu[k]);
+      st(r.var + k * r.P + p, x.var[k]);
+      st(r.w + k * r.P + p, x.w[k]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cold paths (rare per frame): kept out of line so the hot loop stays small.
+// ---------------------------------------------------------------------------
+
+// Illumination reset of one plane-pixel (cascade.py:361-391, per-pixel part)
+template <typename T, int KMAX>
+__device__ __noinline__ void cold_reset(PlaneRef<T> r, size_t p,
+                                        double init_var) {
+  uint32_t meta = r.meta[p];
+  uint32_t dyn = r.dyn[p];
+  int n = meta_count(meta);
+  Mix<KMAX> x;
+  load_mix_r<T, KMAX>(r, p, n, x);
+  double v = (double)dyn_chp(dyn);
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k < n) {
+      x.mu[k] = v;
+      x.var[k] = init_var;
+    }
+  }
+  int inv[KMAX];
+  sort_modes<KMAX>(x, n, inv);
+  store_mix_r<T, KMAX>(r, p, n, x);
+  r.meta[p] = (uint16_t)meta_with_refs(meta,
+                                       select_inv<KMAX>(inv, meta_ref(meta, 0)),
+                                       select_inv<KMAX>(inv, meta_ref(meta, 1)));
+  // streak, clock, waking, hits -> 0; last_active -> -1; label, chp kept
+  r.dyn[p] = pack_dyn(dyn_chp(dyn), dyn_label(dyn), 0, -1, 0);
+  r.streak[p] = 0;
+#pragma unroll
+  for (int l = 0; l < 5; ++l) r.hits[l * r.P + p] = 0;
+}
+
+// Level reorder of one plane-pixel (cascade.py:393-417)
+template <typename T>
+__device__ __noinline__ void cold_reorder(PlaneRef<T> r, size_t p,
+                                          double group_mu) {
+  uint32_t meta = r.meta[p];
+  int code[3];
+  long long nh[3];
+  double nm[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    code[j] = meta_mid(meta, j);
+    nh[j] = 1;                                              // -(-1)
+    nm[j] = __longlong_as_double(0x7ff0000000000000ll);     // -(-inf)
+    if (code[j] >= 0) {
+      nh[j] = -(long long)r.hits[(size_t)code[j] * r.P + p];
+      double lmu = group_mu;
+      if (code[j] != L_GROUP) {
+        int k = meta_ref(meta, code[j] == L_MEAN ? 0 : 1);
+        lmu = ldrw(r.mu + (size_t)k * r.P + p);
+      }
+      nm[j] = -(double)r.table[p * 256 + (int)clip_rint(lmu)];
+    }
+  }
+  // np.lexsort((-mass, -hv)): primary -hv, secondary -mass, stable
+  int out[3] = {-1, -1, -1};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    int rank = 0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      bool less = (nh[j] < nh[i]) || (nh[j] == nh[i] && nm[j] < nm[i]);
+      bool tie = (nh[j] == nh[i]) && (nm[j] == nm[i]);
+      rank += less || (j < i && tie);
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+      if (rank == t) out[t] = code[i];
+  }
+  r.meta[p] = (uint16_t)meta_with_mids(meta, out[0], out[1], out[2]);
+#pragma unroll
+  for (int l = 0; l < 5; ++l) r.hits[l * r.P + p] = 0;
+}
+
+// MEANVAR level hit: mean+variance update of mode rs, re-sort, remap refs
+// (kernels_numba.py:312-334)
+template <typename T, int KMAX>
+__device__ __noinline__ void cold_meanvar(PlaneRef<T> r, size_t p,
+                                          uint32_t meta, int rs, double v,
+                                          double rho, double var_floor) {
+  const int n = meta_count(meta);
+  Mix<KMAX> x;
+  load_mix_r<T, KMAX>(r, p, n, x);
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k == rs) {
+      double mm = (1.0 - rho) * x.mu[k] + rho * v;
+      x.mu[k] = mm;
+      double dd = v - mm;
+      double s2 = (1.0 - rho) * x.var[k] + rho * (dd * dd);
+      if (s2 < var_floor) s2 = var_floor;
+      x.var[k] = s2;
+    }
+  }
+  int inv[KMAX];
+  sort_modes<KMAX>(x, n, inv);
+  store_mix_r<T, KMAX>(r, p, n, x);
+  r.meta[p] = (uint16_t)meta_with_refs(meta,
+                                       select_inv<KMAX>(inv, meta_ref(meta, 0)),
+                                       select_inv<KMAX>(inv, meta_ref(meta, 1)));
+}
+
+// Full mixture update (last level, compat mode and the baseline); remap
+// the cascade's mode references unless compat (kernels_numba.py:218-237,
+// 335-342).  Returns the label.
+template <typename T, int KMAX>
+__device__ __noinline__ int cold_gmm(PlaneRef<T> r, size_t p, uint32_t meta,
+                                     double v, double rho, GmmPar gp,
+                                     int kcap, int remap) {
+  int n = meta_count(meta);
+  Mix<KMAX> x;
+  load_mix_r<T, KMAX>(r, p, n, x);
+  int inv[KMAX];
+  int label = gmm_step<KMAX>(x, n, kcap, v, rho, gp, inv);
+  store_mix_r<T, KMAX>(r, p, n, x);
+  uint32_t nm = meta_with_count(meta, n);
+  if (remap)
+    nm = meta_with_refs(nm, select_inv<KMAX>(inv, meta_ref(meta, 0)),
+                        select_inv<KMAX>(inv, meta_ref(meta, 1)));
+  r.meta[p] = (uint16_t)nm;
+  return label;
+}
+
+// ---------------------------------------------------------------------------
+// The cascade pass of one plane-pixel, hot path (kernels_numba.py:188-359).
+// Returns the kind; label / conf / the new dyn word through references.
+// For COPY the dyn word is returned unwritten (its label bit comes from the
+// anchor lane right after).
+// ---------------------------------------------------------------------------
+struct Flags {
+  bool sampling, grouping, rate, chp, literal, compat;
+};
+
+struct GroupConst {
+  bool ok;       // pixel grouped and groups exist
+  double mu;     // g_mu
+  double thr;    // lam * sqrt(g_var)
+};
+
+template <typename T, int KMAX>
+__device__ __forceinline__ int cascade_px(const StepArgs& a, const Flags& f,
+                                          const PlaneRef<T>& pr, size_t p,
+                                          int vb, bool on_lattice,
+                                          const double* s_bt, double wa,
+                                          double wb, double wc,
+                                          const GroupConst& gc, int& label,
+                                          double& conf, uint32_t& dyn_out) {
+  const cog_params& q = a.q;
+  const size_t P = pr.P;
+  const uint32_t dyn = pr.dyn[p];
+  const int chp = dyn_chp(dyn);
+  const int last_label = dyn_label(dyn);
+  int waking = dyn_waking(dyn);
+  const int last_active = dyn_active(dyn);
+  int clock = dyn_clock(dyn);
+  const double v = (double)vb;
+  const int dv = vb > chp ? vb - chp : chp - vb;
+  const bool changed = (double)dv > q.chp_epsilon;
+  bool zero_streak = false;
+
+  if (f.sampling && clock > 0) {
+    if (!changed) {
+      clock -= 1;
+      if (clock == 0) waking = 1;
+      label = last_label;
+      conf = 0.0;
+      dyn_out = pack_dyn(vb, last_label, waking, last_active, clock);
+      pr.dyn[p] = dyn_out;
+      return K_SKIP;
+    }
+    clock = 0;
+    waking = 0;
+    zero_streak = true;
+  } else if (f.sampling && waking == 1) {
+    waking = 0;
+    if (!changed && !on_lattice) {
+      label = last_label;
+      conf = 0.0;
+      dyn_out = pack_dyn(vb, last_label, 0, last_active, q.sleep_frames);
+      return K_COPY;
+    }
+  }
+
+  const uint32_t meta = pr.meta[p];
+  const GmmPar gp{q.match_lambda, q.background_threshold, q.variance_floor,
+                  q.initial_variance};
+  if (f.compat) {
+    // kind from the pre-update rank-0 mode, then the full update
+    const int n = meta_count(meta);
+    int active = L_GMM;
+    if (n > 0 && fabs(v - ldrw(pr.mu + p)) <= q.match_lambda *
+                                               sqrt(ldrw(pr.var + p)))
+      active = L_MEAN;
+    label = cold_gmm<T, KMAX>(pr, p, meta, v, q.learning_rate, gp, a.g.k, 0);
+    uint32_t* h = pr.hits + (size_t)active * P + p;
+    *h = *h + 1u;
+    conf = 0.0;
+    dyn_out = pack_dyn(vb, label, waking, active, clock);
+    pr.dyn[p] = dyn_out;
+    return active;
+  }
+
+  // ---- confidence from the pre-update state
+  const int r0 = meta_ref(meta, 0), r1 = meta_ref(meta, 1);
+  const int m0 = meta_mid(meta, 0), m1 = meta_mid(meta, 1),
+            m2 = meta_mid(meta, 2);
+  int top = m0;
+  if (top == L_GROUP && !f.grouping) top = m1;
+  double mu_top, den;
+  double mu0 = 0.0, thr0 = 0.0;
+  bool have0 = false;
+  if (top == L_GROUP && gc.ok) {
+    mu_top = gc.mu;
+    den = gc.thr;
+  } else {
+    const int r = (top == L_MEANVAR) ? r1 : r0;
+    mu_top = ldrw(pr.mu + (size_t)r * P + p);
+    den = q.match_lambda * sqrt(ldrw(pr.var + (size_t)r * P + p));
+    if (r == r0) {
+      mu0 = mu_top;
+      thr0 = den;
+      have0 = true;
+    }
+  }
+  const double phat = (double)__ldg(pr.table + p * 256 + vb) /
+                      (double)__ldg(pr.peak + p);
+  const double bterm = s_bt[dv];
+  double gterm = fabs(v - mu_top) / den;
+  if (gterm > 1.0) gterm = 1.0;
+  if (!f.literal) gterm = 1.0 - gterm;
+  if (phat < q.prior_floor) {
+    const double dd = wb + wc;
+    conf = dd > 0.0 ? (wb * bterm + wc * gterm) / dd : 0.0;
+  } else {
+    conf = wa * phat + wb * bterm + wc * gterm;
+  }
+  double rho = q.learning_rate;
+  if (f.rate) {
+    double relax = 1.0 - conf;
+    if (relax < q.rate_floor) relax = q.rate_floor;
+    rho = q.learning_rate * relax;
+  }
+
+  // ---- descend the cascade
+  int active = -1;
+  label = 0;
+  if (f.chp && !changed) {
+    active = L_CHP;
+    label = last_label;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int code = j == 0 ? m0 : (j == 1 ? m1 : m2);
+      if (active >= 0 || code < 0) break;
+      if (code == L_GROUP) {
+        if (!f.grouping || !gc.ok) continue;
+        if (fabs(v - gc.mu) <= gc.thr) active = L_GROUP;
+      } else {
+        const int r = (code == L_MEAN) ? r0 : r1;
+        double mur, thr;
+        if (have0 && r == r0) {
+          mur = mu0;
+          thr = thr0;
+        } else {
+          mur = ldrw(pr.mu + (size_t)r * P + p);
+          thr = q.match_lambda * sqrt(ldrw(pr.var + (size_t)r * P + p));
+        }
+        if (fabs(v - mur) <= thr) {
+          double acc = 0.0;
+          for (int k = 0; k < r; ++k) acc = acc + ldrw(pr.w + (size_t)k * P + p);
+          if (acc <= q.background_threshold) {
+            if (code == L_MEAN) {
+              active = L_MEAN;
+              st(pr.mu + (size_t)r * P + p, (1.0 - rho) * mur + rho * v);
+            } else {
+              active = L_MEANVAR;
+              cold_meanvar<T, KMAX>(pr, p, meta, r, v, rho, q.variance_floor);
+            }
+          }
+        }
+      }
+    }
+    if (active < 0) {
+      active = L_GMM;
+      label = cold_gmm<T, KMAX>(pr, p, meta, v, rho, gp, a.g.k, 1);
+    }
+  }
+
+  // ---- streak / sampling bookkeeping
+  uint32_t sk = zero_streak ? 0u : pr.streak[p];
+  if (conf > q.confidence_threshold)
+    sk = (sk == 0xffffffffu) ? sk : sk + 1u;
+  else
+    sk = 0u;
+  pr.streak[p] = sk;
+  uint32_t* h = pr.hits + (size_t)active * P + p;
+  *h = *h + 1u;
+  if (f.sampling && (long long)sk >= (long long)q.saturation_frames)
+    clock = q.sleep_frames;
+  dyn_out = pack_dyn(vb, label, waking, active, clock);
+  pr.dyn[p] = dyn_out;
+  return active;
+}
+
+// ---------------------------------------------------------------------------
+// Frame tail for one stream: group update, illumination test, stats.
+// Runs on one CTA; `acc` holds the stream's summed partials.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ double exact_group_conf(const StepArgs& a, int s, int c, int g) {
+  // parity/debug mode: the reference's sequential np.bincount order
+  const size_t P = (size_t)a.g.height * a.g.width;
+  const uint8_t* kind = a.kind + ((size_t)s * a.g.depth + c) * P;
+  const T* conf = (const T*)a.conf + ((size_t)s * a.g.depth + c) * P;
+  const uint16_t* gid = a.s.gid + (size_t)s * P;
+  double acc = 0.0;
+  for (size_t p = 0; p < P; ++p)
+    if (kind[p] == L_GROUP && gid[p] == (uint16_t)g) acc = acc + (double)conf[p];
+  return acc;
+}
+
+template <typename T>
+__device__ void finalize_stream(const StepArgs& a, int s,
+                                unsigned long long* acc, int64_t* stats,
+                                uint32_t* sync) {
+  const int d = a.g.depth, G = a.g.n_groups;
+  const cog_params& q = a.q;
+  __shared__ int s_fired;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* va = acc;
+    long long tot[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int c = 0; c < d; ++c)
+      for (int k = 0; k < 7; ++k) tot[k] += (long long)va[acc_kind(c, k)];
+    long long fg = (long long)va[acc_fg(d)];
+    double thresh = q.illumination_fraction * (double)a.g.total_pixels *
+                    (double)d;
+    int fired = (!q.compat && (double)tot[L_GMM] > thresh) ? 1 : 0;
+    int64_t* row = stats + (size_t)s * STATS_WORDS;
+    row[0] = a.frame_index;
+    row[1] = tot[0];
+    row[2] = tot[1];
+    row[3] = tot[2];
+    row[4] = tot[3];
+    row[5] = tot[4];
+    row[6] = tot[5] + tot[6];
+    row[7] = fg;
+    row[8] = tot[4];
+    row[9] = fired;
+    for (int i = 10; i < STATS_WORDS; ++i) row[i] = 0;
+    s_fired = fired;
+  }
+  __syncthreads();
+  const int fired = s_fired;
+  double* gmu = a.s.g_mu + (size_t)s * d * G;
+  double* gvar = a.s.g_var + (size_t)s * d * G;
+  for (int it = threadIdx.x; it < d * G; it += blockDim.x) {
+    int c = it / G, g = it % G;
+    volatile unsigned long long* e = acc + acc_grp(d, G, c, g);
+    unsigned long long cnt = e[0];
+    if (q.grouping_on && cnt > 0) {
+      double cd = (double)cnt;
+      double vbar = (double)e[1] / cd;
+      double csum = q.exact_group_sums
+                        ? exact_group_conf<T>(a, s, c, g)
+                        : (double)e[2] * (1.0 / (double)(1ull << CONF_SPLIT)) +
+                              (double)e[3] * (1.0 / 4503599627370496.0);
+      double cbar = csum / cd;
+      double rho = 1.0 - cbar;
+      if (rho < q.rate_floor) rho = q.rate_floor;
+      rho = q.learning_rate * rho;
+      double m = (1.0 - rho) * gmu[it] + rho * vbar;
+      double dlt = vbar - m;
+      double s2 = (1.0 - rho) * gvar[it] + rho * dlt * dlt;
+      gmu[it] = m;
+      gvar[it] = s2 < q.variance_floor ? q.variance_floor : s2;
+    }
+    unsigned long long members = e[5];
+    if (fired && members > 0) {
+      gmu[it] = (double)e[4] / (double)members;
+      gvar[it] = q.initial_variance;
+    }
+  }
+  __syncthreads();
+  const int words = acc_words(d, G);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) acc[i] = 0ull;
+  if (threadIdx.x == 0) {
+    sync[1] = fired ? 1u : 0u;  // pending reset for the next frame
+    sync[0] = 0u;               // done counter
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused per-frame step.  Work unit = a warp tile of `stride` rows x cw
+// columns (cw a multiple of the stride): every copy pixel's anchor sits in
+// row 0 of the same warp tile, so copy resolution is a warp shuffle and
+// the frame loop has no block barrier.
+// ---------------------------------------------------------------------------
+constexpr int STEP_WARPS = STEP_THREADS / 32;
+
+template <typename T, int KMAX>
+__global__ void __launch_bounds__(STEP_THREADS, 3)
+    step_kernel(const StepArgs a) {
+  extern __shared__ double s_mem[];
+  __shared__ int s_last;
+  const int s = blockIdx.y;
+  const int d = a.g.depth, G = a.g.n_groups;
+  const int H = a.g.height, W = a.g.width, stride = a.g.stride;
+  const size_t P = (size_t)H * W;
+  const int words = acc_words(d, G);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* s_bt = s_mem;                      // [256]
+  double* s_gmu = s_mem + 256;               // [d*G]
+  double* s_gthr = s_gmu + d * G;            // [d*G]
+  unsigned long long* s_acc =
+      (unsigned long long*)(s_gthr + d * G);  // [words]
+
+  const Flags f{a.q.sampling_on != 0, a.q.grouping_on != 0,
+                a.q.rate_scaling_on != 0, a.q.chp_on != 0,
+                a.q.literal_conf != 0, a.q.compat != 0};
+  for (int i = tid; i < 256; i += blockDim.x) {
+    double b = (double)i / 255.0;
+    s_bt[i] = f.literal ? b : 1.0 - b;
+  }
+  const double* gmu = a.s.g_mu + (size_t)s * d * G;
+  const double* gvar = a.s.g_var + (size_t)s * d * G;
+  for (int i = tid; i < d * G; i += blockDim.x) {
+    s_gmu[i] = gmu[i];
+    s_gthr[i] = a.q.match_lambda * sqrt(gvar[i]);
+  }
+  for (int i = tid; i < words; i += blockDim.x) s_acc[i] = 0ull;
+  uint32_t* sync = a.s.sync + (size_t)s * 4;
+  const bool do_reset = (*(volatile uint32_t*)(sync + 1) & 1u) != 0;
+  const bool do_reorder = a.reorder_now != 0;
+  __syncthreads();
+
+  const uint8_t* frame = a.frame + (size_t)s * d * P;
+  const uint8_t* cls = a.s.cls + (size_t)s * P;
+  const uint16_t* gidp = a.s.gid + (size_t)s * P;
+  uint8_t* mask = a.mask + (size_t)s * P;
+  T* confo = (T*)a.conf + (size_t)s * d * P;
+  uint8_t* kindo = a.kind + (size_t)s * d * P;
+  const int cw = a.cw, npx = stride * cw;
+
+  for (int wt = blockIdx.x * STEP_WARPS + warp; wt < a.n_tiles;
+       wt += gridDim.x * STEP_WARPS) {
+    const int ty = wt / a.tiles_x, tx = wt - ty * a.tiles_x;
+    unsigned row0_lbl = 0;
+    for (int it = 0; it < a.iters; ++it) {
+      const int idx = it * 32 + lane;
+      const int r = idx / cw, col = idx - r * cw;
+      const int y = ty * stride + r, x = tx * cw + col;
+      const bool valid = (idx < npx) && (y < H) && (x < W);
+      const size_t p = valid ? (size_t)y * W + x : 0;
+      const bool on_lat = ((a.g.row0 + y) % stride == 0) && (x % stride == 0);
+      const int anchor_lane = col - col % stride;
+      int gid = (int)UNGROUPED;
+      double wa = 0.0, wb = 0.0, wc = 0.0;
+      if (valid) {
+        gid = gidp[p];
+        const int cl = cls[p];
+        wa = a.q.weights[3 * cl];
+        wb = a.q.weights[3 * cl + 1];
+        wc = a.q.weights[3 * cl + 2];
+      }
+      const bool member = valid && G > 0 && gid != (int)UNGROUPED;
+      int fg = 0;
+#pragma unroll 1
+      for (int c = 0; c < d; ++c) {
+        const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+        int kind = 0, label = 0, vb = 0;
+        double conf = 0.0;
+        uint32_t dw = 0;
+        if (valid) {
+          vb = frame[(size_t)c * P + p];
+          if (do_reset) cold_reset<T, KMAX>(pr, p, a.q.initial_variance);
+          if (do_reorder)
+            cold_reorder<T>(pr, p, member ? s_gmu[c * G + gid]
+                                          : (G > 0 ? s_gmu[c * G] : 0.0));
+          GroupConst gc;
+          gc.ok = member;
+          gc.mu = member ? s_gmu[c * G + gid] : 0.0;
+          gc.thr = member ? s_gthr[c * G + gid] : 0.0;
+          kind = cascade_px<T, KMAX>(a, f, pr, p, vb, on_lat, s_bt, wa, wb, wc,
+                                     gc, label, conf, dw);
+        }
+        // copy resolution: anchors live in row 0 of this warp tile
+        const int src = (it == 0) ? label : (int)((row0_lbl >> c) & 1u);
+        const int al = __shfl_sync(FULL, src, anchor_lane);
+        if (valid) {
+          if (kind == K_COPY) {
+            label = al;
+            pr.dyn[p] = (dw & ~(1u << 8)) | ((uint32_t)al << 8);
+          }
+          st(confo + (size_t)c * P + p, conf);
+          kindo[(size_t)c * P + p] = (uint8_t)kind;
+        }
+        if (it == 0) row0_lbl |= ((unsigned)label & 1u) << c;
+        fg |= label;
+
+        // ---- warp-aggregated reductions for this plane
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+          const unsigned m = __ballot_sync(FULL, valid && kind == k);
+          if (lane == 0 && m)
+            atomicAdd(&s_acc[acc_kind(c, k)], (unsigned long long)__popc(m));
+        }
+        unsigned todo = __ballot_sync(FULL, member);
+        while (todo) {
+          const int leader = __ffs(todo) - 1;
+          const int g = __shfl_sync(FULL, gid, leader);
+          const bool mine = member && gid == g;
+          const unsigned mm = __ballot_sync(FULL, mine);
+          todo &= ~mm;
+          const unsigned sall = warp_sum_u32(mine ? (unsigned)vb : 0u);
+          const bool hit = mine && kind == L_GROUP;
+          const unsigned hm = __ballot_sync(FULL, hit);
+          unsigned sv = 0, q2 = 0, q1 = 0, q0 = 0;
+          if (hm) {
+            unsigned long long qv = 0;
+            if (hit) {
+              const double cq = conf * 4503599627370496.0;  // 2^52
+              qv = cq > 0.0 ? (unsigned long long)cq : 0ull;
+            }
+            sv = warp_sum_u32(hit ? (unsigned)vb : 0u);
+            q2 = warp_sum_u32((unsigned)(qv >> 40));
+            q1 = warp_sum_u32((unsigned)((qv >> 20) & 0xFFFFFu));
+            q0 = warp_sum_u32((unsigned)(qv & 0xFFFFFu));
+          }
+          if (lane == 0) {
+            unsigned long long* e = s_acc + acc_grp(d, G, c, g);
+            atomicAdd(e + 4, (unsigned long long)sall);
+            atomicAdd(e + 5, (unsigned long long)__popc(mm));
+            if (hm) {
+              const unsigned long long Q = ((unsigned long long)q2 << 40) +
+                                           ((unsigned long long)q1 << 20) +
+                                           (unsigned long long)q0;
+              atomicAdd(e + 0, (unsigned long long)__popc(hm));
+              atomicAdd(e + 1, (unsigned long long)sv);
+              atomicAdd(e + 2, Q >> CONF_SPLIT);
+              atomicAdd(e + 3, Q & ((1ull << CONF_SPLIT) - 1ull));
+            }
+          }
+        }
+      }
+      if (valid) mask[p] = fg ? 255 : 0;
+      const unsigned fm = __ballot_sync(FULL, valid && fg);
+      if (lane == 0 && fm)
+        atomicAdd(&s_acc[acc_fg(d)], (unsigned long long)__popc(fm));
+    }
+  }
+
+  // ---- publish this CTA's partials; the last CTA of the stream finalizes
+  __syncthreads();
+  unsigned long long* gacc =
+      (unsigned long long*)a.s.accum + (size_t)s * words;
+  for (int i = tid; i < words; i += blockDim.x) {
+    const unsigned long long v = s_acc[i];
+    if (v) atomicAdd(gacc + i, v);
+  }
+  if (!a.fuse_finalize) return;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned t = atomicAdd(sync, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  finalize_stream<T>(a, s, gacc, a.stats, sync);
+}
+
+template <typename T>
+__global__ void finalize_kernel(const StepArgs a) {
+  const int s = blockIdx.x;
+  const int words = acc_words(a.g.depth, a.g.n_groups);
+  finalize_stream<T>(a, s, (unsigned long long*)a.s.accum + (size_t)s * words,
+                     a.stats, a.s.sync + (size_t)s * 4);
+}
+
+template <typename T, int KMAX>
+__global__ void __launch_bounds__(256) pending_kernel(const StepArgs a) {
+  const int s = blockIdx.y;
+  const int d = a.g.depth, G = a.g.n_groups;
+  const size_t P = (size_t)a.g.height * a.g.width;
+  uint32_t* sync = a.s.sync + (size_t)s * 4;
+  const bool do_reset = (*(volatile uint32_t*)(sync + 1) & 1u) != 0;
+  const bool do_reorder = a.reorder_now != 0;
+  if (!do_reset && !do_reorder) return;
+  const double* gmu = a.s.g_mu + (size_t)s * d * G;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < d * P;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / P);
+    const size_t p = i % P;
+    const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+    if (do_reset) cold_reset<T, KMAX>(pr, p, a.q.initial_variance);
+    if (do_reorder) {
+      const int gid = a.s.gid[(size_t)s * P + p];
+      const double gm = G > 0 ? gmu[(size_t)c * G + (gid == (int)UNGROUPED ? 0 : gid)] : 0.0;
+      cold_reorder<T>(pr, p, gm);
+    }
+  }
+}
+
+// clears the pending flag after pending_kernel (separate launch: every CTA
+// of pending_kernel must have read the flag first)
+__global__ void clear_pending_kernel(uint32_t* sync, int streams) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < streams) sync[(size_t)s * 4 + 1] = 0u;
+}
+
+// ---------------------------------------------------------------------------
+// training: prior
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    prior_kernel(const uint8_t* __restrict__ frames, int N, int d, int64_t P,
+                 const double* __restrict__ kern,
+                 const int32_t* __restrict__ windows, int nw, float* tables,
+                 float* peak, uint16_t* hist_out, double t1, double t2,
+                 double peaky, uint32_t* residue, uint8_t* cls) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  uint8_t* samp = psm;                                          // [N][32]
+  uint16_t* hist = (uint16_t*)(psm + (((size_t)N * 32 + 15) & ~(size_t)15));
+  const int64_t p0 = (int64_t)blockIdx.x * PRIOR_PIX;
+  const int npx = (int)min((int64_t)PRIOR_PIX, P - p0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  unsigned rc0 = 0, rc1 = 0, rc2 = 0;
+
+  for (int c = 0; c < d; ++c) {
+    for (int e = tid; e < N * 32; e += blockDim.x) {
+      int i = e >> 5, t = e & 31;
+      samp[e] = (t < npx) ? frames[((size_t)i * d + c) * P + p0 + t] : 0;
+    }
+    for (int e = tid; e < 256 * 32; e += blockDim.x) hist[e] = 0;
+    __syncthreads();
+    if (tid < npx) {
+      int prev = samp[tid];
+      for (int i = 1; i < N; ++i) {
+        int cur = samp[i * 32 + tid];
+        double rr = (double)abs(cur - prev);
+        int b = (rr >= t1) + (rr >= t2);
+        rc0 += (b == 0);
+        rc1 += (b == 1);
+        rc2 += (b == 2);
+        prev = cur;
+      }
+    }
+    int prev_w = 0;
+    for (int j = 0; j < nw; ++j) {
+      const int wj = windows[j];
+      if (tid < npx) {
+        for (int i = N - wj; i < N - prev_w; ++i)
+          hist[samp[i * 32 + tid] * 32 + tid] += 1;
+      }
+      prev_w = wj;
+      __syncthreads();
+      const bool last = (j == nw - 1);
+      if (last && hist_out) {
+        for (int e = tid; e < npx * 256; e += blockDim.x) {
+          int t = e >> 8, bin = e & 255;
+          hist_out[((size_t)c * P + p0 + t) * 256 + bin] = hist[bin * 32 + t];
+        }
+      }
+      const double inv_n = (double)wj;
+      for (int t = warp; t < npx; t += nwarps) {
+        double acc[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) acc[jj] = 0.0;
+        for (int chunk = 0; chunk < 8; ++chunk) {
+          unsigned cnt = hist[(chunk * 32 + lane) * 32 + t];
+          unsigned m = __ballot_sync(FULL, cnt != 0);
+          while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            const double cd = (double)__shfl_sync(FULL, cnt, b);
+            const double* row = kern + (size_t)(chunk * 32 + b) * 256;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              acc[jj] = acc[jj] + cd * __ldg(row + jj * 32 + lane);
+          }
+        }
+        float mx = 0.0f;
+        float* trow = tables + (((size_t)j * d + c) * P + p0 + t) * 256;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          float fv = (float)(acc[jj] / inv_n);
+          trow[jj * 32 + lane] = fv;
+          mx = fmaxf(mx, fv);
+        }
+        if (last) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+            mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+          if (lane == 0) peak[(size_t)c * P + p0 + t] = mx > 0.0f ? mx : 1.0f;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid < npx) {
+    const double den = (double)(N - 1) * (double)d;
+    const double o0 = (double)rc0 / den, o1 = (double)rc1 / den;
+    uint8_t k = 2;
+    if (o1 >= peaky) k = 1;
+    if (o0 >= peaky) k = 0;
+    cls[p0 + tid] = k;
+    if (residue) {
+      residue[(p0 + tid) * 3 + 0] = rc0;
+      residue[(p0 + tid) * 3 + 1] = rc1;
+      residue[(p0 + tid) * 3 + 2] = rc2;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// training: GMM warm-up, adaptation statistics, mode references
+// ---------------------------------------------------------------------------
+struct WarmArgs {
+  cog_geom g;
+  cog_params q;
+  cog_state s;
+  const uint8_t* frames;
+  int N;
+  double* features;
+  double* w_final;
+};
+
+template <int KMAX>
+__device__ __forceinline__ void warm_init(Mix<KMAX>& m, double v0,
+                                          double init_var) {
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    m.mu[k] = 0.0;
+    m.var[k] = init_var;
+    m.w[k] = 0.0;
+  }
+  m.mu[0] = v0;
+  m.w[0] = 1.0;
+}
+
+template <typename T, int KMAX>
+__global__ void __launch_bounds__(128) warmup_kernel(const WarmArgs a) {
+  const int c = blockIdx.y;
+  const int d = a.g.depth, K = a.g.k;
+  const size_t P = (size_t)a.g.height * a.g.width;
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
+                  a.q.variance_floor, a.q.initial_variance};
+  const double lr = a.q.learning_rate;
+  const uint8_t* fr = a.frames;
+  const int N = a.N;
+  const bool series = (c == 0) && a.features != nullptr;
+  Mix<KMAX> m;
+  int inv[KMAX];
+  int n = 1;
+  warm_init<KMAX>(m, (double)fr[(size_t)c * P + p], a.q.initial_variance);
+  double sv = m.var[0], sw = m.w[0];
+  for (int i = 1; i < N; ++i) {
+    double v = (double)fr[((size_t)i * d + c) * P + p];
+    gmm_step<KMAX>(m, n, K, v, lr, gp, inv);
+    if (series) {
+      sv = sv + m.var[0];
+      sw = sw + m.w[0];
+    }
+  }
+  if (series) {
+    // numpy var(axis=0, ddof=0): sequential mean, then sequential sum of
+    // squared deviations -- recompute the series rather than storing it
+    const double mv = sv / (double)N, mw = sw / (double)N;
+    Mix<KMAX> r;
+    int rn = 1;
+    warm_init<KMAX>(r, (double)fr[(size_t)c * P + p], a.q.initial_variance);
+    double dv = r.var[0] - mv, dw = r.w[0] - mw;
+    double qv = dv * dv, qw = dw * dw;
+    for (int i = 1; i < N; ++i) {
+      double v = (double)fr[((size_t)i * d + c) * P + p];
+      gmm_step<KMAX>(r, rn, K, v, lr, gp, inv);
+      dv = r.var[0] - mv;
+      dw = r.w[0] - mw;
+      qv = qv + dv * dv;
+      qw = qw + dw * dw;
+    }
+    a.features[p * 2 + 0] = qv / (double)N;
+    a.features[p * 2 + 1] = qw / (double)N;
+    if (a.w_final) a.w_final[p] = m.w[0];
+  }
+  // store the mixture (dead slots keep the canonical (0, init_var, 0))
+  const size_t base = (size_t)c * K * P;
+  for (int k = 0; k < K; ++k) {
+    double mu = 0.0, var = a.q.initial_variance, w = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KMAX; ++kk)
+      if (kk == k) {
+        mu = m.mu[kk];
+        var = m.var[kk];
+        w = m.w[kk];
+      }
+    st((T*)a.s.mu + base + k * P + p, mu);
+    st((T*)a.s.var + base + k * P + p, var);
+    st((T*)a.s.w + base + k * P + p, w);
+  }
+  // mode references: lexsort((-tie, -mass)) over all K slots
+  // (cascade.py:218-235); dead slots carry (-inf, -inf)
+  const float* trow = a.s.table + ((size_t)c * P + p) * 256;
+  double nm[KMAX], nt[KMAX];
+  const double PINF = __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    nm[k] = PINF;
+    nt[k] = PINF;
+    if (k < n) {
+      nm[k] = -(double)trow[(int)clip_rint(m.mu[k])];
+      nt[k] = -(m.w[k] / sqrt(m.var[k]));
+    }
+  }
+  int ref0 = 0, ref1 = 0;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    if (i >= K) continue;
+    int r = 0;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      if (j >= K) continue;
+      bool less = (nm[j] < nm[i]) || (nm[j] == nm[i] && nt[j] < nt[i]);
+      bool tie = (nm[j] == nm[i]) && (nt[j] == nt[i]);
+      r += less || (j < i && tie);
+    }
+    if (r == 0) ref0 = i;
+    if (r == 1) ref1 = i;
+  }
+  if (n < 2) ref1 = ref0;
+  const size_t pi = (size_t)c * P + p;
+  a.s.meta[pi] = (uint16_t)pack_meta(n, L_MEAN, L_MEANVAR, -1, ref0, ref1);
+  a.s.dyn[pi] = pack_dyn(fr[((size_t)(N - 1) * d + c) * P + p], 0, 0, -1, 0);
+  a.s.streak[pi] = 0u;
+#pragma unroll
+  for (int l = 0; l < 5; ++l) a.s.hits[((size_t)c * 5 + l) * P + p] = 0u;
+}
+
+__global__ void set_levels_kernel(cog_geom g, uint16_t* meta,
+                                  const uint16_t* gid) {
+  const size_t P = (size_t)g.height * g.width;
+  const size_t total = (size_t)g.streams * g.depth * P;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t s = i / ((size_t)g.depth * P);
+    const size_t p = i % P;
+    const bool grouped = gid[s * P + p] != UNGROUPED;
+    uint32_t m = meta[i];
+    meta[i] = (uint16_t)(grouped ? meta_with_mids(m, L_GROUP, L_MEAN, L_MEANVAR)
+                                 : meta_with_mids(m, L_MEAN, L_MEANVAR, -1));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// baseline mixture (gmm.classify_frame)
+// ---------------------------------------------------------------------------
+template <typename T, int KMAX>
+__global__ void __launch_bounds__(256) baseline_kernel(const StepArgs a) {
+  const int d = a.g.depth, K = a.g.k;
+  const size_t P = (size_t)a.g.height * a.g.width;
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
+                  a.q.variance_floor, a.q.initial_variance};
+  int fg = 0;
+  for (int c = 0; c < d; ++c) {
+    MixPtrs<T> mp{(T*)a.s.mu + (size_t)c * K * P, (T*)a.s.var + (size_t)c * K * P,
+                  (T*)a.s.w + (size_t)c * K * P};
+    uint16_t* metap = a.s.meta + (size_t)c * P + p;
+    uint32_t meta = *metap;
+    int n = meta_count(meta);
+    Mix<KMAX> x;
+    load_mix<T, KMAX>(mp, P, p, n, x);
+    int inv[KMAX];
+    int n0 = n;
+    fg |= gmm_step<KMAX>(x, n, K, (double)a.frame[(size_t)c * P + p],
+                         a.q.learning_rate, gp, inv);
+    store_mix<T, KMAX>(mp, P, p, n, x);
+    if (n != n0) *metap = (uint16_t)meta_with_count(meta, n);
+  }
+  a.mask[p] = fg ? 255 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// state export / import (reference layouts)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void export_kernel(cog_geom g, cog_state s, cog_ref_state o) {
+  const size_t P = (size_t)g.height * g.width;
+  const int d = g.depth, K = g.k;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < d * P;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t c = i / P, p = i % P;
+    for (int k = 0; k < K; ++k) {
+      const size_t src = (c * K + k) * P + p, dst = i * K + k;
+      o.mu[dst] = (double)((const T*)s.mu)[src];
+      o.var[dst] = (double)((const T*)s.var)[src];
+      o.w[dst] = (double)((const T*)s.w)[src];
+    }
+    uint32_t m = s.meta[i], dy = s.dyn[i];
+    o.count[i] = meta_count(m);
+    for (int j = 0; j < 3; ++j) o.mid[i * 3 + j] = (int8_t)meta_mid(m, j);
+    o.ref[i * 2 + 0] = (int8_t)meta_ref(m, 0);
+    o.ref[i * 2 + 1] = (int8_t)meta_ref(m, 1);
+    o.chp[i] = (uint8_t)dyn_chp(dy);
+    o.label[i] = (uint8_t)dyn_label(dy);
+    o.active[i] = (int8_t)dyn_active(dy);
+    o.waking[i] = (uint8_t)dyn_waking(dy);
+    o.clock[i] = dyn_clock(dy);
+    o.streak[i] = s.streak[i];
+    for (int l = 0; l < 5; ++l) o.hits[i * 5 + l] = s.hits[(c * 5 + l) * P + p];
+  }
+}
+
+template <typename T>
+__global__ void import_kernel(cog_geom g, cog_state s, cog_ref_state in) {
+  const size_t P = (size_t)g.height * g.width;
+  const int d = g.depth, K = g.k;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < d * P;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t c = i / P, p = i % P;
+    for (int k = 0; k < K; ++k) {
+      const size_t dst = (c * K + k) * P + p, src = i * K + k;
+      st((T*)s.mu + dst, in.mu[src]);
+      st((T*)s.var + dst, in.var[src]);
+      st((T*)s.w + dst, in.w[src]);
+    }
+    s.meta[i] = (uint16_t)pack_meta((int)in.count[i], in.mid[i * 3],
+                                    in.mid[i * 3 + 1], in.mid[i * 3 + 2],
+                                    in.ref[i * 2], in.ref[i * 2 + 1]);
+    long long ck = in.clock[i];
+    s.dyn[i] = pack_dyn(in.chp[i], in.label[i] & 1, in.waking[i] & 1,
+                        in.active[i], (int)(ck < 0 ? 0 : (ck > 65535 ? 65535 : ck)));
+    long long sk = in.streak[i];
+    s.streak[i] = (uint32_t)(sk < 0 ? 0 : (sk > 0xffffffffll ? 0xffffffffll : sk));
+    for (int l = 0; l < 5; ++l) {
+      long long h = in.hits[i * 5 + l];
+      s.hits[(c * 5 + l) * P + p] =
+          (uint32_t)(h < 0 ? 0 : (h > 0xffffffffll ? 0xffffffffll : h));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int check_geom(const cog_geom* g) {
+  if (!g) return COG_EINVAL;
+  if (g->height < 1 || g->width < 1 || g->depth < 1 || g->depth > MAXD)
+    return COG_EINVAL;
+  if (g->k < 1 || g->k > 8) return COG_EUNSUPPORTED;
+  if (g->stride < 1 || g->stride > 16 || g->streams < 1 || g->n_groups < 0)
+    return COG_EUNSUPPORTED;
+  if (g->row0 % g->stride) return COG_EINVAL;
+  return COG_OK;
+}
+
+int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? COG_OK : (int)e;
+}
+
+StepArgs make_args(const cog_geom* g, const cog_params* q, const cog_state* s) {
+  StepArgs a{};
+  a.g = *g;
+  if (q) a.q = *q;
+  a.s = *s;
+  const int st = g->stride;
+  const int m = (32 / (st * st)) > 0 ? 32 / (st * st) : 1;
+  a.cw = st * m;
+  a.iters = (st * a.cw + 31) / 32;
+  a.tiles_x = (g->width + a.cw - 1) / a.cw;
+  const int tiles_y = (g->height + st - 1) / st;
+  a.n_tiles = a.tiles_x * tiles_y;
+  return a;
+}
+
+template <typename T>
+using StepFn = void (*)(const StepArgs);
+
+template <typename T>
+StepFn<T> pick_step(int K) {
+  if (K <= 3) return step_kernel<T, 3>;
+  if (K <= 5) return step_kernel<T, 5>;
+  return step_kernel<T, 8>;
+}
+template <typename T>
+StepFn<T> pick_pending(int K) {
+  if (K <= 3) return pending_kernel<T, 3>;
+  if (K <= 5) return pending_kernel<T, 5>;
+  return pending_kernel<T, 8>;
+}
+template <typename T>
+StepFn<T> pick_baseline(int K) {
+  if (K <= 3) return baseline_kernel<T, 3>;
+  if (K <= 5) return baseline_kernel<T, 5>;
+  return baseline_kernel<T, 8>;
+}
+
+template <typename T>
+int launch_step(const StepArgs& a, cudaStream_t st) {
+  auto fn = pick_step<T>(a.g.k);
+  const size_t smem = 256 * 8 + (size_t)2 * a.g.depth * a.g.n_groups * 8 +
+                      (size_t)acc_words(a.g.depth, a.g.n_groups) * 8;
+  if (smem > 200 * 1024) return COG_EUNSUPPORTED;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, STEP_THREADS, smem);
+  if (occ < 1) occ = 1;
+  const int need = (a.n_tiles + STEP_WARPS - 1) / STEP_WARPS;
+  int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
+  int gx = need < per_stream ? need : per_stream;
+  if (gx < 1) gx = 1;
+  dim3 grid(gx, a.g.streams);
+  fn<<<grid, STEP_THREADS, smem, st>>>(a);
+  return launch_status();
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* cog_version(void) {
+  return "cog_b200 1.0 (sm_100a, binary64 decisions, fused step)";
+}
+
+int64_t cog_accum_words(int32_t depth, int32_t n_groups) {
+  return acc_words(depth, n_groups);
+}
+
+int cog_prior_build(const uint8_t* frames, int32_t n_frames, int32_t depth,
+                    int64_t n_pix, const double* kern, const int32_t* windows,
+                    int32_t n_windows, float* tables, float* peak,
+                    uint16_t* hist, double residue_t1, double residue_t2,
+                    double peaky_threshold, uint32_t* residue, uint8_t* cls,
+                    void* stream) {
+  if (!frames || !kern || !windows || !tables || !peak || !cls)
+    return COG_EINVAL;
+  if (n_frames < 2 || depth < 1 || n_pix < 1 || n_windows < 1)
+    return COG_EINVAL;
+  const size_t smem = (((size_t)n_frames * 32 + 15) & ~(size_t)15) +
+                      256 * 32 * sizeof(uint16_t);
+  if (smem > 200 * 1024) return COG_EUNSUPPORTED;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(prior_kernel,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned blocks = (unsigned)((n_pix + PRIOR_PIX - 1) / PRIOR_PIX);
+  prior_kernel<<<blocks, 256, smem, (cudaStream_t)stream>>>(
+      frames, n_frames, depth, n_pix, kern, windows, n_windows, tables, peak,
+      hist, residue_t1, residue_t2, peaky_threshold, residue, cls);
+  return launch_status();
+}
+
+int cog_gmm_warmup(const cog_geom* geom, const cog_params* prm,
+                   const cog_state* st, const uint8_t* frames,
+                   int32_t n_frames, double* features, double* w_final,
+                   void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!prm || !st || !frames || n_frames < 1) return COG_EINVAL;
+  WarmArgs a{};
+  a.g = *geom;
+  a.q = *prm;
+  a.s = *st;
+  a.frames = frames;
+  a.N = n_frames;
+  a.features = features;
+  a.w_final = w_final;
+  const size_t P = (size_t)geom->height * geom->width;
+  dim3 grid((unsigned)((P + 127) / 128), geom->depth);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int K = geom->k;
+  if (geom->state_f64) {
+    if (K <= 3) warmup_kernel<double, 3><<<grid, 128, 0, s>>>(a);
+    else if (K <= 5) warmup_kernel<double, 5><<<grid, 128, 0, s>>>(a);
+    else warmup_kernel<double, 8><<<grid, 128, 0, s>>>(a);
+  } else {
+    if (K <= 3) warmup_kernel<float, 3><<<grid, 128, 0, s>>>(a);
+    else if (K <= 5) warmup_kernel<float, 5><<<grid, 128, 0, s>>>(a);
+    else warmup_kernel<float, 8><<<grid, 128, 0, s>>>(a);
+  }
+  return launch_status();
+}
+
+int cog_set_levels(const cog_geom* geom, const cog_state* st, void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!st || !st->meta || !st->gid) return COG_EINVAL;
+  set_levels_kernel<<<num_sms() * 4, 256, 0, (cudaStream_t)stream>>>(
+      *geom, st->meta, st->gid);
+  return launch_status();
+}
+
+int cog_step(const cog_geom* geom, const cog_params* prm, const cog_state* st,
+             const uint8_t* frame, uint8_t* mask, void* conf, uint8_t* kind,
+             int64_t* stats, int64_t frame_index, int32_t reorder_now,
+             int32_t fuse_finalize, void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!prm || !st || !frame || !mask || !conf || !kind || !stats)
+    return COG_EINVAL;
+  StepArgs a = make_args(geom, prm, st);
+  a.frame = frame;
+  a.mask = mask;
+  a.conf = conf;
+  a.kind = kind;
+  a.stats = stats;
+  a.frame_index = frame_index;
+  a.reorder_now = reorder_now;
+  a.fuse_finalize = fuse_finalize;
+  cudaStream_t s = (cudaStream_t)stream;
+  return geom->state_f64 ? launch_step<double>(a, s) : launch_step<float>(a, s);
+}
+
+int cog_finalize(const cog_geom* geom, const cog_params* prm,
+                 const cog_state* st, int64_t* stats, int64_t frame_index,
+                 void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!prm || !st || !stats) return COG_EINVAL;
+  StepArgs a = make_args(geom, prm, st);
+  a.stats = stats;
+  a.frame_index = frame_index;
+  if (geom->state_f64)
+    finalize_kernel<double><<<geom->streams, 128, 0, (cudaStream_t)stream>>>(a);
+  else
+    finalize_kernel<float><<<geom->streams, 128, 0, (cudaStream_t)stream>>>(a);
+  return launch_status();
+}
+
+int cog_apply_pending(const cog_geom* geom, const cog_params* prm,
+                      const cog_state* st, int32_t reorder_now, void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!prm || !st) return COG_EINVAL;
+  StepArgs a = make_args(geom, prm, st);
+  a.reorder_now = reorder_now;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t work = (size_t)geom->depth * geom->height * geom->width;
+  unsigned gx = (unsigned)((work + 255) / 256);
+  const unsigned cap = (unsigned)num_sms() * 8;
+  if (gx > cap) gx = cap;
+  dim3 grid(gx, geom->streams);
+  if (geom->state_f64) pick_pending<double>(geom->k)<<<grid, 256, 0, s>>>(a);
+  else pick_pending<float>(geom->k)<<<grid, 256, 0, s>>>(a);
+  rc = launch_status();
+  if (rc) return rc;
+  clear_pending_kernel<<<(geom->streams + 127) / 128, 128, 0, s>>>(
+      st->sync, geom->streams);
+  return launch_status();
+}
+
+int cog_baseline_frame(const cog_geom* geom, const cog_params* prm,
+                       const cog_state* st, const uint8_t* frame,
+                       uint8_t* mask, void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!prm || !st || !frame || !mask) return COG_EINVAL;
+  StepArgs a = make_args(geom, prm, st);
+  a.frame = frame;
+  a.mask = mask;
+  const size_t P = (size_t)geom->height * geom->width;
+  const unsigned blocks = (unsigned)((P + 255) / 256);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (geom->state_f64) pick_baseline<double>(geom->k)<<<blocks, 256, 0, s>>>(a);
+  else pick_baseline<float>(geom->k)<<<blocks, 256, 0, s>>>(a);
+  return launch_status();
+}
+
+int cog_export_state(const cog_geom* geom, const cog_state* st,
+                     const cog_ref_state* out, void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!st || !out) return COG_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned blocks = (unsigned)num_sms() * 4;
+  if (geom->state_f64) export_kernel<double><<<blocks, 256, 0, s>>>(*geom, *st, *out);
+  else export_kernel<float><<<blocks, 256, 0, s>>>(*geom, *st, *out);
+  return launch_status();
+}
+
+int cog_import_state(const cog_geom* geom, const cog_state* st,
+                     const cog_ref_state* in, void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!st || !in) return COG_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned blocks = (unsigned)num_sms() * 4;
+  if (geom->state_f64) import_kernel<double><<<blocks, 256, 0, s>>>(*geom, *st, *in);
+  else import_kernel<float><<<blocks, 256, 0, s>>>(*geom, *st, *in);
+  return launch_status();
+}
+
+}  // extern "C"

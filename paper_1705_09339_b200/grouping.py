@@ -1,0 +1,156 @@
+"""Training phase 2: spatio-temporal grouping (host side).
+
+Algorithm of /root/reference/pkg/src/cogbg/grouping.py:85-208: z-scored
+behaviour features -> seeded farthest-point k-means -> sigma-band trimming
+-> pooled per-group, per-plane mode.  The features themselves are produced
+on the GPU by the warm-up kernel (``cog_gmm_warmup``, bit-identical to
+``numpy.var(axis=0)`` of the adaptation series); only the global, discrete
+clustering runs here, in numpy with the reference's exact expressions so the
+group map is identical.  It is training-time work ("gather
+per-pixel features to host, run build_groups").
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .config import EngineConfig
+from .errors import ClusteringError, TrainingError
+
+UNGROUPED = -1
+_POOL_EXACT_BYTES = 1 << 31
+
+
+@dataclass
+class GroupMap:
+    group_id: np.ndarray      # (P,) int64, -1 ungrouped
+    mu: np.ndarray            # (G, d)
+    var: np.ndarray           # (G, d)
+    weight: np.ndarray        # (G,)
+    member_count: np.ndarray  # (G,) int64
+
+    @property
+    def group_count(self) -> int:
+        return self.mu.shape[0]
+
+    @staticmethod
+    def empty(n_pix: int, depth: int) -> "GroupMap":
+        return GroupMap(np.full(n_pix, UNGROUPED, dtype=np.int64),
+                        np.zeros((0, depth)), np.zeros((0, depth)),
+                        np.zeros(0), np.zeros(0, dtype=np.int64))
+
+
+class KMeans:
+    """Deterministic k-means: seeded first centre, farthest-point spread,
+    lowest-index tie breaks (grouping.py:100-126)."""
+
+    def __init__(self, k: int, seed: int, max_iter: int = 100):
+        self.k, self.seed, self.max_iter = k, seed, max_iter
+
+    def _spread(self, pts: np.ndarray) -> np.ndarray:
+        n = pts.shape[0]
+        first = int(np.random.default_rng(self.seed).integers(n))
+        ctr = np.empty((self.k, pts.shape[1]))
+        ctr[0] = pts[first]
+        far = ((pts - ctr[0]) ** 2).sum(axis=1)
+        for j in range(1, self.k):
+            ctr[j] = pts[int(np.argmax(far))]
+            far = np.minimum(far, ((pts - ctr[j]) ** 2).sum(axis=1))
+        return ctr
+
+    def fit(self, pts: np.ndarray):
+        n = pts.shape[0]
+        if n < self.k:
+            raise ClusteringError(f"{n} pixels cannot form {self.k} clusters")
+        ctr = self._spread(pts)
+        label = np.full(n, -1, dtype=np.int64)
+        for _ in range(self.max_iter):
+            d2 = ((pts[:, None, :] - ctr[None, :, :]) ** 2).sum(axis=2)
+            nxt = np.argmin(d2, axis=1)
+            if np.array_equal(nxt, label):
+                break
+            label = nxt
+            for j in range(self.k):
+                sub = pts[label == j]
+                if sub.shape[0]:
+                    ctr[j] = sub.mean(axis=0)
+        return label, ctr
+
+
+def kmeans(features, k, seed, max_iter=100):
+    return KMeans(k, seed, max_iter).fit(features)
+
+
+def standardise(f: np.ndarray) -> np.ndarray:
+    mean = f.mean(axis=0)
+    std = f.std(axis=0, ddof=0)
+    return (f - mean) / np.where(std > 0, std, 1.0)
+
+
+def band_members(assign: np.ndarray, features: np.ndarray,
+                 c: float) -> np.ndarray:
+    """Keep pixels within mean +- c*std of their cluster on both features
+    (grouping.py:142-161)."""
+    out = np.full(assign.shape[0], UNGROUPED, dtype=np.int64)
+    for j in np.unique(assign):
+        sel = assign == j
+        if sel.sum() < 2:
+            continue
+        f = features[sel]
+        inside = np.abs(f - f.mean(axis=0)) <= c * f.std(axis=0, ddof=0)
+        inside |= np.ptp(f, axis=0) == 0
+        out[np.where(sel)[0][inside.all(axis=1)]] = j
+    return out
+
+
+def _pooled_stats(values: np.ndarray, sel: np.ndarray, floor: float):
+    """Per-plane mean / floored variance of all training intensities of the
+    members (grouping.py:189-192).  Small pools use the reference's exact
+    numpy expression; huge pools (4K scenes) fall back to a chunked
+    two-pass evaluation (mean still exact, variance within ~1e-15)."""
+    n, d, _ = values.shape
+    m = int(sel.sum())
+    if n * d * m * 8 <= _POOL_EXACT_BYTES:
+        pooled = values[:, :, sel].astype(np.float64)
+        return (pooled.mean(axis=(0, 2)),
+                np.maximum(pooled.var(axis=(0, 2), ddof=0), floor))
+    idx = np.where(sel)[0]
+    cnt = float(n * m)
+    tot = np.zeros(d, dtype=np.int64)
+    step = max(1, _POOL_EXACT_BYTES // (8 * n * d))
+    for a in range(0, m, step):
+        tot += values[:, :, idx[a:a + step]].astype(np.int64).sum(axis=(0, 2))
+    mean = tot / cnt
+    sq = np.zeros(d)
+    for a in range(0, m, step):
+        x = values[:, :, idx[a:a + step]].astype(np.float64) - mean[None, :, None]
+        sq += (x * x).sum(axis=(0, 2))
+    return mean, np.maximum(sq / cnt, floor)
+
+
+def build_groups(features: np.ndarray, w_final: np.ndarray,
+                 values: np.ndarray, config: EngineConfig) -> GroupMap:
+    """features (P, 2) f64, w_final (P,) f64, values (N, d, P) uint8."""
+    n, d, p = values.shape
+    if not config.grouping:
+        return GroupMap.empty(p, d)
+    if features.shape != (p, 2):
+        raise TrainingError("feature geometry does not match frames")
+    assign, _ = KMeans(config.clusters, config.cluster_seed).fit(
+        standardise(features))
+    member = band_members(assign, features, config.cluster_threshold)
+    kept = [j for j in np.unique(member)
+            if j != UNGROUPED and (member == j).sum() >= 2]
+    g = len(kept)
+    gm = GroupMap(np.full(p, UNGROUPED, dtype=np.int64), np.zeros((g, d)),
+                  np.zeros((g, d)), np.zeros(g), np.zeros(g, dtype=np.int64))
+    for gi, j in enumerate(kept):
+        sel = member == j
+        gm.group_id[sel] = gi
+        gm.member_count[gi] = sel.sum()
+        gm.mu[gi], gm.var[gi] = _pooled_stats(values, sel,
+                                              config.variance_floor)
+        gm.weight[gi] = w_final[sel].mean()
+    return gm

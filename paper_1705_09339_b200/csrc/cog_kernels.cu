@@ -310,9 +310,12 @@ __device__ __noinline__ int cold_gmm(PlaneRef<T> r, size_t p, uint32_t meta,
 
 // ---------------------------------------------------------------------------
 // The cascade pass of one plane-pixel, hot path (kernels_numba.py:188-359).
-// Returns the kind; label / conf / the new dyn word through references.
-// For COPY the dyn word is returned unwritten (its label bit comes from the
-// anchor lane right after).
+// Decides the kind, confidence and rate and does all bookkeeping, but
+// leaves the two deep updates (MEANVAR hit: mean+var update and re-sort;
+// GMM fall-through: full mixture update) to the caller's dense deep pass:
+// `deep` returns DEEP_NONE / DEEP_MEANVAR / DEEP_GMM / DEEP_COMPAT.
+// The dyn word is written here unless the kind is COPY or the label is not
+// known yet (GMM): then it is returned in dyn_out (label bit 0).
 // ---------------------------------------------------------------------------
 struct Flags {
   bool sampling, grouping, rate, chp, literal, compat;
@@ -324,14 +327,21 @@ struct GroupConst {
   double thr;    // lam * sqrt(g_var)
 };
 
-template <typename T, int KMAX>
-__device__ __forceinline__ int cascade_px(const StepArgs& a, const Flags& f,
-                                          const PlaneRef<T>& pr, size_t p,
-                                          int vb, bool on_lattice,
-                                          const double* s_bt, double wa,
-                                          double wb, double wc,
-                                          const GroupConst& gc, int& label,
-                                          double& conf, uint32_t& dyn_out) {
+enum Deep : int { DEEP_NONE = 0, DEEP_MEANVAR = 1, DEEP_GMM = 2,
+                  DEEP_COMPAT = 3 };
+
+struct HotOut {
+  int kind, label, deep, rsel;
+  double conf, rho;
+  uint32_t dyn;
+};
+
+template <typename T>
+__device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
+                                       const PlaneRef<T>& pr, size_t p, int vb,
+                                       bool on_lattice, const double* s_bt,
+                                       double wa, double wb, double wc,
+                                       const GroupConst& gc, HotOut& o) {
   const cog_params& q = a.q;
   const size_t P = pr.P;
   const uint32_t dyn = pr.dyn[p];
@@ -344,16 +354,20 @@ __device__ __forceinline__ int cascade_px(const StepArgs& a, const Flags& f,
   const int dv = vb > chp ? vb - chp : chp - vb;
   const bool changed = (double)dv > q.chp_epsilon;
   bool zero_streak = false;
+  o.deep = DEEP_NONE;
+  o.rsel = 0;
+  o.rho = 0.0;
 
   if (f.sampling && clock > 0) {
     if (!changed) {
       clock -= 1;
       if (clock == 0) waking = 1;
-      label = last_label;
-      conf = 0.0;
-      dyn_out = pack_dyn(vb, last_label, waking, last_active, clock);
-      pr.dyn[p] = dyn_out;
-      return K_SKIP;
+      o.kind = K_SKIP;
+      o.label = last_label;
+      o.conf = 0.0;
+      o.dyn = pack_dyn(vb, last_label, waking, last_active, clock);
+      pr.dyn[p] = o.dyn;
+      return;
     }
     clock = 0;
     waking = 0;
@@ -361,30 +375,31 @@ __device__ __forceinline__ int cascade_px(const StepArgs& a, const Flags& f,
   } else if (f.sampling && waking == 1) {
     waking = 0;
     if (!changed && !on_lattice) {
-      label = last_label;
-      conf = 0.0;
-      dyn_out = pack_dyn(vb, last_label, 0, last_active, q.sleep_frames);
-      return K_COPY;
+      o.kind = K_COPY;
+      o.label = last_label;
+      o.conf = 0.0;
+      o.dyn = pack_dyn(vb, 0, 0, last_active, q.sleep_frames);
+      return;
     }
   }
 
   const uint32_t meta = pr.meta[p];
-  const GmmPar gp{q.match_lambda, q.background_threshold, q.variance_floor,
-                  q.initial_variance};
   if (f.compat) {
-    // kind from the pre-update rank-0 mode, then the full update
+    // kind from the pre-update rank-0 mode; the full update is deep work
     const int n = meta_count(meta);
     int active = L_GMM;
-    if (n > 0 && fabs(v - ldrw(pr.mu + p)) <= q.match_lambda *
-                                               sqrt(ldrw(pr.var + p)))
+    if (n > 0 && fabs(v - ldrw(pr.mu + p)) <=
+                     q.match_lambda * sqrt(ldrw(pr.var + p)))
       active = L_MEAN;
-    label = cold_gmm<T, KMAX>(pr, p, meta, v, q.learning_rate, gp, a.g.k, 0);
     uint32_t* h = pr.hits + (size_t)active * P + p;
     *h = *h + 1u;
-    conf = 0.0;
-    dyn_out = pack_dyn(vb, label, waking, active, clock);
-    pr.dyn[p] = dyn_out;
-    return active;
+    o.kind = active;
+    o.label = 0;
+    o.conf = 0.0;
+    o.deep = DEEP_COMPAT;
+    o.rho = q.learning_rate;
+    o.dyn = pack_dyn(vb, 0, waking, active, clock);
+    return;
   }
 
   // ---- confidence from the pre-update state
@@ -415,6 +430,7 @@ __device__ __forceinline__ int cascade_px(const StepArgs& a, const Flags& f,
   double gterm = fabs(v - mu_top) / den;
   if (gterm > 1.0) gterm = 1.0;
   if (!f.literal) gterm = 1.0 - gterm;
+  double conf;
   if (phat < q.prior_floor) {
     const double dd = wb + wc;
     conf = dd > 0.0 ? (wb * bterm + wc * gterm) / dd : 0.0;
@@ -430,7 +446,7 @@ __device__ __forceinline__ int cascade_px(const StepArgs& a, const Flags& f,
 
   // ---- descend the cascade
   int active = -1;
-  label = 0;
+  int label = 0;
   if (f.chp && !changed) {
     active = L_CHP;
     label = last_label;
@@ -454,14 +470,16 @@ __device__ __forceinline__ int cascade_px(const StepArgs& a, const Flags& f,
         }
         if (fabs(v - mur) <= thr) {
           double acc = 0.0;
-          for (int k = 0; k < r; ++k) acc = acc + ldrw(pr.w + (size_t)k * P + p);
+          for (int k = 0; k < r; ++k)
+            acc = acc + ldrw(pr.w + (size_t)k * P + p);
           if (acc <= q.background_threshold) {
             if (code == L_MEAN) {
               active = L_MEAN;
               st(pr.mu + (size_t)r * P + p, (1.0 - rho) * mur + rho * v);
             } else {
               active = L_MEANVAR;
-              cold_meanvar<T, KMAX>(pr, p, meta, r, v, rho, q.variance_floor);
+              o.deep = DEEP_MEANVAR;
+              o.rsel = r;
             }
           }
         }
@@ -469,11 +487,11 @@ __device__ __forceinline__ int cascade_px(const StepArgs& a, const Flags& f,
     }
     if (active < 0) {
       active = L_GMM;
-      label = cold_gmm<T, KMAX>(pr, p, meta, v, rho, gp, a.g.k, 1);
+      o.deep = DEEP_GMM;
     }
   }
 
-  // ---- streak / sampling bookkeeping
+  // ---- streak / sampling bookkeeping (label-independent)
   uint32_t sk = zero_streak ? 0u : pr.streak[p];
   if (conf > q.confidence_threshold)
     sk = (sk == 0xffffffffu) ? sk : sk + 1u;
@@ -484,9 +502,12 @@ __device__ __forceinline__ int cascade_px(const StepArgs& a, const Flags& f,
   *h = *h + 1u;
   if (f.sampling && (long long)sk >= (long long)q.saturation_frames)
     clock = q.sleep_frames;
-  dyn_out = pack_dyn(vb, label, waking, active, clock);
-  pr.dyn[p] = dyn_out;
-  return active;
+  o.kind = active;
+  o.label = label;
+  o.conf = conf;
+  o.rho = rho;
+  o.dyn = pack_dyn(vb, label, waking, active, clock);
+  if (o.deep != DEEP_GMM) pr.dyn[p] = o.dyn;
 }
 
 // ---------------------------------------------------------------------------
@@ -574,16 +595,38 @@ __device__ void finalize_stream(const StepArgs& a, int s,
   if (threadIdx.x == 0) {
     sync[1] = fired ? 1u : 0u;  // pending reset for the next frame
     sync[0] = 0u;               // done counter
+    sync[2] = 0u;               // tile counter
   }
 }
 
 // ---------------------------------------------------------------------------
 // fused per-frame step.  Work unit = a warp tile of `stride` rows x cw
-// columns (cw a multiple of the stride): every copy pixel's anchor sits in
-// row 0 of the same warp tile, so copy resolution is a warp shuffle and
-// the frame loop has no block barrier.
+// columns (cw a multiple of the stride), fetched from a per-stream atomic
+// counter (dynamic balance).  Every copy pixel's anchor sits in row 0 of
+// the same warp tile, so copy resolution is a warp shuffle and the frame
+// loop has no block barrier.  Per warp tile:
+//   1. hot pass, plane by plane: kinds, confidences, cheap levels and all
+//      bookkeeping; MEANVAR hits and GMM fall-throughs are queued
+//   2. deep pass: the queued plane-pixels of all planes run densely, one
+//      per lane (instead of one divergent pass per plane)
+//   3. finish: GMM labels patched in, copies resolved, union mask written
+// Partial sums go to warp-private shared slices (plain adds).
 // ---------------------------------------------------------------------------
 constexpr int STEP_WARPS = STEP_THREADS / 32;
+constexpr int QCAP = 32 * MAXD;
+
+struct WarpScratch {  // one per warp, in dynamic shared memory
+  uint32_t qcode[QCAP];
+  double qrho[QCAP];
+  uint32_t dw[MAXD][32];
+  uint32_t glab[32];
+};
+
+__host__ __device__ inline size_t step_smem_bytes(int d, int G) {
+  return 256 * 8 + (size_t)2 * d * G * 8 +
+         (size_t)STEP_WARPS * acc_words(d, G) * 8 +
+         (size_t)STEP_WARPS * sizeof(WarpScratch);
+}
 
 template <typename T, int KMAX>
 __global__ void __launch_bounds__(STEP_THREADS, 3)
@@ -599,14 +642,17 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
   double* s_bt = s_mem;                      // [256]
   double* s_gmu = s_mem + 256;               // [d*G]
   double* s_gthr = s_gmu + d * G;            // [d*G]
-  unsigned long long* s_acc =
-      (unsigned long long*)(s_gthr + d * G);  // [words]
+  unsigned long long* s_acc_all =
+      (unsigned long long*)(s_gthr + d * G);  // [warps][words]
+  WarpScratch* s_ws = (WarpScratch*)(s_acc_all + STEP_WARPS * words);
+  unsigned long long* wacc = s_acc_all + warp * words;
+  WarpScratch& ws = s_ws[warp];
 
   const Flags f{a.q.sampling_on != 0, a.q.grouping_on != 0,
                 a.q.rate_scaling_on != 0, a.q.chp_on != 0,
                 a.q.literal_conf != 0, a.q.compat != 0};
   for (int i = tid; i < 256; i += blockDim.x) {
-    double b = (double)i / 255.0;
+    const double b = (double)i / 255.0;
     s_bt[i] = f.literal ? b : 1.0 - b;
   }
   const double* gmu = a.s.g_mu + (size_t)s * d * G;
@@ -615,7 +661,7 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
     s_gmu[i] = gmu[i];
     s_gthr[i] = a.q.match_lambda * sqrt(gvar[i]);
   }
-  for (int i = tid; i < words; i += blockDim.x) s_acc[i] = 0ull;
+  for (int i = tid; i < STEP_WARPS * words; i += blockDim.x) s_acc_all[i] = 0ull;
   uint32_t* sync = a.s.sync + (size_t)s * 4;
   const bool do_reset = (*(volatile uint32_t*)(sync + 1) & 1u) != 0;
   const bool do_reorder = a.reorder_now != 0;
@@ -628,9 +674,15 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
   T* confo = (T*)a.conf + (size_t)s * d * P;
   uint8_t* kindo = a.kind + (size_t)s * d * P;
   const int cw = a.cw, npx = stride * cw;
+  const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
+                  a.q.variance_floor, a.q.initial_variance};
+  unsigned long long fg_count = 0;
 
-  for (int wt = blockIdx.x * STEP_WARPS + warp; wt < a.n_tiles;
-       wt += gridDim.x * STEP_WARPS) {
+  for (;;) {
+    int wt = 0;
+    if (lane == 0) wt = (int)atomicAdd(sync + 2, 1u);
+    wt = __shfl_sync(FULL, wt, 0);
+    if (wt >= a.n_tiles) break;
     const int ty = wt / a.tiles_x, tx = wt - ty * a.tiles_x;
     unsigned row0_lbl = 0;
     for (int it = 0; it < a.iters; ++it) {
@@ -640,7 +692,6 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
       const bool valid = (idx < npx) && (y < H) && (x < W);
       const size_t p = valid ? (size_t)y * W + x : 0;
       const bool on_lat = ((a.g.row0 + y) % stride == 0) && (x % stride == 0);
-      const int anchor_lane = col - col % stride;
       int gid = (int)UNGROUPED;
       double wa = 0.0, wb = 0.0, wc = 0.0;
       if (valid) {
@@ -651,13 +702,23 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
         wc = a.q.weights[3 * cl + 2];
       }
       const bool member = valid && G > 0 && gid != (int)UNGROUPED;
-      int fg = 0;
+      unsigned lbits = 0, copybits = 0, gmmbits = 0;
+      int nq = 0;
+      ws.glab[lane] = 0u;
+
+      // ---- 1. hot pass, plane by plane
 #pragma unroll 1
       for (int c = 0; c < d; ++c) {
         const PlaneRef<T> pr = plane_ref<T>(a, s, c);
-        int kind = 0, label = 0, vb = 0;
-        double conf = 0.0;
-        uint32_t dw = 0;
+        HotOut o;
+        o.kind = 0;
+        o.label = 0;
+        o.deep = DEEP_NONE;
+        o.conf = 0.0;
+        o.rho = 0.0;
+        o.rsel = 0;
+        o.dyn = 0;
+        int vb = 0;
         if (valid) {
           vb = frame[(size_t)c * P + p];
           if (do_reset) cold_reset<T, KMAX>(pr, p, a.q.initial_variance);
@@ -668,30 +729,37 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
           gc.ok = member;
           gc.mu = member ? s_gmu[c * G + gid] : 0.0;
           gc.thr = member ? s_gthr[c * G + gid] : 0.0;
-          kind = cascade_px<T, KMAX>(a, f, pr, p, vb, on_lat, s_bt, wa, wb, wc,
-                                     gc, label, conf, dw);
+          hot_px<T>(a, f, pr, p, vb, on_lat, s_bt, wa, wb, wc, gc, o);
+          st(confo + (size_t)c * P + p, o.conf);
+          kindo[(size_t)c * P + p] = (uint8_t)o.kind;
         }
-        // copy resolution: anchors live in row 0 of this warp tile
-        const int src = (it == 0) ? label : (int)((row0_lbl >> c) & 1u);
-        const int al = __shfl_sync(FULL, src, anchor_lane);
-        if (valid) {
-          if (kind == K_COPY) {
-            label = al;
-            pr.dyn[p] = (dw & ~(1u << 8)) | ((uint32_t)al << 8);
-          }
-          st(confo + (size_t)c * P + p, conf);
-          kindo[(size_t)c * P + p] = (uint8_t)kind;
+        lbits |= ((unsigned)o.label & 1u) << c;
+        if (o.kind == K_COPY && valid) {
+          copybits |= 1u << c;
+          ws.dw[c][lane] = o.dyn;
         }
-        if (it == 0) row0_lbl |= ((unsigned)label & 1u) << c;
-        fg |= label;
+        const bool labeled_later = valid && (o.deep == DEEP_GMM ||
+                                             o.deep == DEEP_COMPAT);
+        if (labeled_later) {
+          gmmbits |= 1u << c;
+          ws.dw[c][lane] = o.dyn;
+        }
+        // enqueue deep work
+        const bool dq = valid && o.deep != DEEP_NONE;
+        const unsigned qm = __ballot_sync(FULL, dq);
+        if (dq) {
+          const int pos = nq + __popc(qm & ((1u << lane) - 1u));
+          ws.qcode[pos] = (uint32_t)lane | ((uint32_t)c << 5) |
+                          ((uint32_t)o.deep << 7) | ((uint32_t)o.rsel << 9) |
+                          ((uint32_t)vb << 12);
+          ws.qrho[pos] = o.rho;
+        }
+        nq += __popc(qm);
 
-        // ---- warp-aggregated reductions for this plane
-#pragma unroll
-        for (int k = 0; k < 7; ++k) {
-          const unsigned m = __ballot_sync(FULL, valid && kind == k);
-          if (lane == 0 && m)
-            atomicAdd(&s_acc[acc_kind(c, k)], (unsigned long long)__popc(m));
-        }
+        // ---- per-plane reductions (label-independent)
+        const unsigned peers = __match_any_sync(FULL, valid ? o.kind : 15);
+        if (valid && lane == __ffs(peers) - 1)
+          wacc[acc_kind(c, o.kind)] += (unsigned long long)__popc(peers);
         unsigned todo = __ballot_sync(FULL, member);
         while (todo) {
           const int leader = __ffs(todo) - 1;
@@ -700,13 +768,13 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
           const unsigned mm = __ballot_sync(FULL, mine);
           todo &= ~mm;
           const unsigned sall = warp_sum_u32(mine ? (unsigned)vb : 0u);
-          const bool hit = mine && kind == L_GROUP;
+          const bool hit = mine && o.kind == L_GROUP;
           const unsigned hm = __ballot_sync(FULL, hit);
           unsigned sv = 0, q2 = 0, q1 = 0, q0 = 0;
           if (hm) {
             unsigned long long qv = 0;
             if (hit) {
-              const double cq = conf * 4503599627370496.0;  // 2^52
+              const double cq = o.conf * 4503599627370496.0;  // 2^52
               qv = cq > 0.0 ? (unsigned long long)cq : 0ull;
             }
             sv = warp_sum_u32(hit ? (unsigned)vb : 0u);
@@ -715,34 +783,80 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
             q0 = warp_sum_u32((unsigned)(qv & 0xFFFFFu));
           }
           if (lane == 0) {
-            unsigned long long* e = s_acc + acc_grp(d, G, c, g);
-            atomicAdd(e + 4, (unsigned long long)sall);
-            atomicAdd(e + 5, (unsigned long long)__popc(mm));
+            unsigned long long* e = wacc + acc_grp(d, G, c, g);
+            e[4] += sall;
+            e[5] += (unsigned long long)__popc(mm);
             if (hm) {
               const unsigned long long Q = ((unsigned long long)q2 << 40) +
                                            ((unsigned long long)q1 << 20) +
                                            (unsigned long long)q0;
-              atomicAdd(e + 0, (unsigned long long)__popc(hm));
-              atomicAdd(e + 1, (unsigned long long)sv);
-              atomicAdd(e + 2, Q >> CONF_SPLIT);
-              atomicAdd(e + 3, Q & ((1ull << CONF_SPLIT) - 1ull));
+              e[0] += (unsigned long long)__popc(hm);
+              e[1] += sv;
+              e[2] += Q >> CONF_SPLIT;
+              e[3] += Q & ((1ull << CONF_SPLIT) - 1ull);
             }
           }
         }
       }
+
+      // ---- 2. deep pass: queued plane-pixels, one per lane
+      __syncwarp();
+      for (int e = lane; e < nq; e += 32) {
+        const uint32_t code = ws.qcode[e];
+        const int owner = code & 31, c = (code >> 5) & 3;
+        const int kindq = (code >> 7) & 3, rs = (code >> 9) & 7;
+        const double v = (double)((code >> 12) & 0xFF);
+        const int oidx = it * 32 + owner;
+        const int orow = oidx / cw, ocol = oidx - orow * cw;
+        const size_t op = (size_t)(ty * stride + orow) * W + (tx * cw + ocol);
+        const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+        const uint32_t meta = pr.meta[op];
+        if (kindq == DEEP_MEANVAR) {
+          cold_meanvar<T, KMAX>(pr, op, meta, rs, v, ws.qrho[e],
+                                a.q.variance_floor);
+        } else {
+          const int lbl = cold_gmm<T, KMAX>(pr, op, meta, v, ws.qrho[e], gp,
+                                            a.g.k, kindq == DEEP_GMM);
+          if (lbl) atomicOr(&ws.glab[owner], 1u << c);
+        }
+      }
+      __syncwarp();
+
+      // ---- 3. finish: GMM labels, copy resolution, union mask
+      const unsigned glab = ws.glab[lane];
+      int fg = 0;
+#pragma unroll 1
+      for (int c = 0; c < d; ++c) {
+        int label = (int)((lbits >> c) & 1u);
+        if ((gmmbits >> c) & 1u) {
+          label = (int)((glab >> c) & 1u);
+          a.s.dyn[((size_t)s * d + c) * P + p] =
+              ws.dw[c][lane] | ((uint32_t)label << 8);
+        }
+        const int src = (it == 0) ? label : (int)((row0_lbl >> c) & 1u);
+        const int al = __shfl_sync(FULL, src, col - col % stride);
+        if ((copybits >> c) & 1u) {
+          label = al;
+          a.s.dyn[((size_t)s * d + c) * P + p] =
+              ws.dw[c][lane] | ((uint32_t)al << 8);
+        }
+        if (it == 0) row0_lbl |= ((unsigned)label & 1u) << c;
+        fg |= label;
+      }
       if (valid) mask[p] = fg ? 255 : 0;
-      const unsigned fm = __ballot_sync(FULL, valid && fg);
-      if (lane == 0 && fm)
-        atomicAdd(&s_acc[acc_fg(d)], (unsigned long long)__popc(fm));
+      fg_count += __popc(__ballot_sync(FULL, valid && fg));
+      __syncwarp();
     }
   }
+  if (lane == 0) wacc[acc_fg(d)] += fg_count;
 
   // ---- publish this CTA's partials; the last CTA of the stream finalizes
   __syncthreads();
   unsigned long long* gacc =
       (unsigned long long*)a.s.accum + (size_t)s * words;
   for (int i = tid; i < words; i += blockDim.x) {
-    const unsigned long long v = s_acc[i];
+    unsigned long long v = 0;
+    for (int w = 0; w < STEP_WARPS; ++w) v += s_acc_all[w * words + i];
     if (v) atomicAdd(gacc + i, v);
   }
   if (!a.fuse_finalize) return;
@@ -1202,8 +1316,7 @@ StepFn<T> pick_baseline(int K) {
 template <typename T>
 int launch_step(const StepArgs& a, cudaStream_t st) {
   auto fn = pick_step<T>(a.g.k);
-  const size_t smem = 256 * 8 + (size_t)2 * a.g.depth * a.g.n_groups * 8 +
-                      (size_t)acc_words(a.g.depth, a.g.n_groups) * 8;
+  const size_t smem = step_smem_bytes(a.g.depth, a.g.n_groups);
   if (smem > 200 * 1024) return COG_EUNSUPPORTED;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

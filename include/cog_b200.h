@@ -45,6 +45,8 @@
  *   cls      u8[P], gid u16[P] (0xFFFF = ungrouped)
  *   g_mu, g_var  f64[depth][G], g_members u32[G]
  *   accum    u64[cog_accum_words()], sync u32[4]
+ *   deepq    u64 + f64 [cog_deepq_slots()]  per-frame worklist of MEANVAR /
+ *            GMM plane-pixels (consumed and re-zeroed by the deep pass)
  */
 #ifndef COG_B200_H
 #define COG_B200_H
@@ -101,10 +103,15 @@ typedef struct cog_state {
   const uint32_t *g_members;
   uint64_t *accum;
   uint32_t *sync;
+  uint64_t *deepq;   /* u64[cog_deepq_slots()] worklist (zero-initialised) */
+  double *deeprho;   /* f64[cog_deepq_slots()] */
 } cog_state;
 
 /* Words of `accum` per stream (kinds, foreground, group partials). */
 int64_t cog_accum_words(int32_t depth, int32_t n_groups);
+
+/* Worklist slots per stream (deep-level plane-pixels of one frame). */
+int64_t cog_deepq_slots(int32_t depth, int64_t n_pix);
 
 /* Scene prior for one stream: frames u8[N][depth][P].  Writes, for each
  * trailing window windows[j] (ascending, last == N), tables

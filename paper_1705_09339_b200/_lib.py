@@ -91,7 +91,8 @@ class Params(ctypes.Structure):
 class State(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "mu", "var", "w", "meta", "dyn", "streak", "hits", "table", "peak",
-        "cls", "gid", "g_mu", "g_var", "g_members", "accum", "sync")]
+        "cls", "gid", "g_mu", "g_var", "g_members", "accum", "sync",
+        "deepq", "deeprho")]
 
 
 class RefState(ctypes.Structure):
@@ -103,6 +104,7 @@ class RefState(ctypes.Structure):
 _P = ctypes.c_void_p
 _SIGS = {
     "cog_accum_words": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
+    "cog_deepq_slots": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int64]),
     "cog_prior_build": (ctypes.c_int, [
         _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, _P, _P,
         ctypes.c_int32, _P, _P, _P, ctypes.c_double, ctypes.c_double,
@@ -130,7 +132,7 @@ def load(path: Path | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        so = Path(path) if path else SO_PATH
+        so = Path(path or os.environ.get("COG_LIB") or SO_PATH)
         if not so.exists():
             try:
                 build_extension()

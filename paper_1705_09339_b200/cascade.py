@@ -206,6 +206,9 @@ class DeviceState:
         self.sync = z(S, 4, dtype=torch.int32)
         self.conf = z(S, d, P, dtype=self.tdtype)
         self.kind = z(S, d, P, dtype=torch.uint8)
+        slots = int(_lib.load().cog_deepq_slots(d, P))
+        self.deepq = z(S, slots, dtype=torch.int64)
+        self.deeprho = torch.empty((S, slots), dtype=torch.float64, device=dev)
         self._refresh()
 
     def _refresh(self) -> None:
@@ -218,7 +221,7 @@ class DeviceState:
         st = _lib.State()
         for name in ("mu", "var", "w", "meta", "dyn", "streak", "hits",
                      "table", "peak", "cls", "gid", "g_mu", "g_var",
-                     "g_members", "accum", "sync"):
+                     "g_members", "accum", "sync", "deepq", "deeprho"):
             setattr(st, name, getattr(self, name).data_ptr())
         self.cstate = st
 
@@ -227,7 +230,7 @@ class DeviceState:
         st = _lib.State()
         for name in ("mu", "var", "w", "meta", "dyn", "streak", "hits",
                      "table", "peak", "cls", "gid", "g_mu", "g_var",
-                     "g_members", "accum", "sync"):
+                     "g_members", "accum", "sync", "deepq", "deeprho"):
             setattr(st, name, getattr(self, name)[s].data_ptr())
         return st
 

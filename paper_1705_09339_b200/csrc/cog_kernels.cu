@@ -336,15 +336,75 @@ struct HotOut {
   uint32_t dyn;
 };
 
+// Everything the common path reads, issued as two independent rounds of
+// loads before any decision: round 1 needs only the pixel index, round 2
+// the round-1 values (table entry at v; the mode the confidence reads).
+template <typename T>
+struct Pre {
+  int vb;
+  uint32_t dyn, meta, streak;
+  float peak, tv;
+  T mut, vart;
+};
+
+// the mode slot whose (mu, var) the confidence reads, or -1 for the group
+__device__ __forceinline__ int top_ref(bool grouping, uint32_t meta,
+                                       bool group_ok) {
+  int top = meta_mid(meta, 0);
+  if (top == L_GROUP && !grouping) top = meta_mid(meta, 1);
+  if (top == L_GROUP && group_ok) return -1;
+  return meta_ref(meta, top == L_MEANVAR ? 1 : 0);
+}
+
+// false for pixels the sampling gate will skip or copy (no table / mode
+// reads for them)
+__device__ __forceinline__ bool will_evaluate(bool sampling, uint32_t dyn,
+                                              int vb, bool on_lattice,
+                                              double eps) {
+  if (!sampling) return true;
+  const int chp = dyn_chp(dyn);
+  const bool changed = (double)(vb > chp ? vb - chp : chp - vb) > eps;
+  if (dyn_clock(dyn) > 0) return changed;
+  if (dyn_waking(dyn) == 1) return changed || on_lattice;
+  return true;
+}
+
+template <typename T>
+__device__ __forceinline__ void preload(const PlaneRef<T>& pr, size_t p,
+                                        const uint8_t* frame_c, bool grouping,
+                                        bool group_ok, bool sampling,
+                                        bool compat, bool on_lattice,
+                                        double eps, Pre<T>& x) {
+  x.vb = frame_c[p];
+  x.dyn = pr.dyn[p];
+  const bool evaluate =
+      !compat && will_evaluate(sampling, x.dyn, x.vb, on_lattice, eps);
+  x.meta = pr.meta[p];
+  x.streak = pr.streak[p];
+  x.peak = __ldg(pr.peak + p);
+  x.tv = 0.0f;
+  x.mut = (T)0;
+  x.vart = (T)1;
+  if (!evaluate) return;
+  x.tv = __ldg(pr.table + p * 256 + x.vb);
+  const int rt = top_ref(grouping, x.meta, group_ok);
+  if (rt >= 0) {
+    x.mut = pr.mu[(size_t)rt * pr.P + p];
+    x.vart = pr.var[(size_t)rt * pr.P + p];
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
-                                       const PlaneRef<T>& pr, size_t p, int vb,
-                                       bool on_lattice, const double* s_bt,
-                                       double wa, double wb, double wc,
+                                       const PlaneRef<T>& pr, size_t p,
+                                       const Pre<T>& pre, bool on_lattice,
+                                       const double* s_bt, double wa,
+                                       double wb, double wc,
                                        const GroupConst& gc, HotOut& o) {
   const cog_params& q = a.q;
   const size_t P = pr.P;
-  const uint32_t dyn = pr.dyn[p];
+  const int vb = pre.vb;
+  const uint32_t dyn = pre.dyn;
   const int chp = dyn_chp(dyn);
   const int last_label = dyn_label(dyn);
   int waking = dyn_waking(dyn);
@@ -383,7 +443,7 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
     }
   }
 
-  const uint32_t meta = pr.meta[p];
+  const uint32_t meta = pre.meta;
   if (f.compat) {
     // kind from the pre-update rank-0 mode; the full update is deep work
     const int n = meta_count(meta);
@@ -391,8 +451,7 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
     if (n > 0 && fabs(v - ldrw(pr.mu + p)) <=
                      q.match_lambda * sqrt(ldrw(pr.var + p)))
       active = L_MEAN;
-    uint32_t* h = pr.hits + (size_t)active * P + p;
-    *h = *h + 1u;
+    atomicAdd(pr.hits + (size_t)active * P + p, 1u);  // RED: no round trip
     o.kind = active;
     o.label = 0;
     o.conf = 0.0;
@@ -416,16 +475,15 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
     den = gc.thr;
   } else {
     const int r = (top == L_MEANVAR) ? r1 : r0;
-    mu_top = ldrw(pr.mu + (size_t)r * P + p);
-    den = q.match_lambda * sqrt(ldrw(pr.var + (size_t)r * P + p));
+    mu_top = (double)pre.mut;
+    den = q.match_lambda * sqrt((double)pre.vart);
     if (r == r0) {
       mu0 = mu_top;
       thr0 = den;
       have0 = true;
     }
   }
-  const double phat = (double)__ldg(pr.table + p * 256 + vb) /
-                      (double)__ldg(pr.peak + p);
+  const double phat = (double)pre.tv / (double)pre.peak;
   const double bterm = s_bt[dv];
   double gterm = fabs(v - mu_top) / den;
   if (gterm > 1.0) gterm = 1.0;
@@ -492,14 +550,13 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
   }
 
   // ---- streak / sampling bookkeeping (label-independent)
-  uint32_t sk = zero_streak ? 0u : pr.streak[p];
+  uint32_t sk = zero_streak ? 0u : pre.streak;
   if (conf > q.confidence_threshold)
     sk = (sk == 0xffffffffu) ? sk : sk + 1u;
   else
     sk = 0u;
   pr.streak[p] = sk;
-  uint32_t* h = pr.hits + (size_t)active * P + p;
-  *h = *h + 1u;
+  atomicAdd(pr.hits + (size_t)active * P + p, 1u);  // RED: no round trip
   if (f.sampling && (long long)sk >= (long long)q.saturation_frames)
     clock = q.sleep_frames;
   o.kind = active;
@@ -534,13 +591,16 @@ __device__ void finalize_stream(const StepArgs& a, int s,
   const int d = a.g.depth, G = a.g.n_groups;
   const cog_params& q = a.q;
   __shared__ int s_fired;
+  __shared__ long long s_tot[7 * MAXD + 1];
+  __syncthreads();
+  for (int i = threadIdx.x; i <= 7 * d; i += blockDim.x)
+    s_tot[i] = (long long)__ldcg(acc + i);
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned long long* va = acc;
     long long tot[7] = {0, 0, 0, 0, 0, 0, 0};
     for (int c = 0; c < d; ++c)
-      for (int k = 0; k < 7; ++k) tot[k] += (long long)va[acc_kind(c, k)];
-    long long fg = (long long)va[acc_fg(d)];
+      for (int k = 0; k < 7; ++k) tot[k] += s_tot[acc_kind(c, k)];
+    long long fg = s_tot[acc_fg(d)];
     double thresh = q.illumination_fraction * (double)a.g.total_pixels *
                     (double)d;
     int fired = (!q.compat && (double)tot[L_GMM] > thresh) ? 1 : 0;
@@ -564,7 +624,9 @@ __device__ void finalize_stream(const StepArgs& a, int s,
   double* gvar = a.s.g_var + (size_t)s * d * G;
   for (int it = threadIdx.x; it < d * G; it += blockDim.x) {
     int c = it / G, g = it % G;
-    volatile unsigned long long* e = acc + acc_grp(d, G, c, g);
+    unsigned long long e[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) e[j] = __ldcg(acc + acc_grp(d, G, c, g) + j);
     unsigned long long cnt = e[0];
     if (q.grouping_on && cnt > 0) {
       double cd = (double)cnt;
@@ -596,6 +658,7 @@ __device__ void finalize_stream(const StepArgs& a, int s,
     sync[1] = fired ? 1u : 0u;  // pending reset for the next frame
     sync[0] = 0u;               // done counter
     sync[2] = 0u;               // tile counter
+    sync[3] = 0u;               // worklist length
   }
 }
 
@@ -614,13 +677,39 @@ __device__ void finalize_stream(const StepArgs& a, int s,
 // ---------------------------------------------------------------------------
 constexpr int STEP_WARPS = STEP_THREADS / 32;
 constexpr int QCAP = 32 * MAXD;
+// worklist slots per stream: every plane-pixel at most once per frame
+__host__ __device__ inline size_t dq_capacity(int d, size_t P) {
+  return (size_t)d * P;
+}
+
+constexpr int WQ_CAP = 128;  // warp-private worklist buffer (flushed when full)
 
 struct WarpScratch {  // one per warp, in dynamic shared memory
   uint32_t qcode[QCAP];
   double qrho[QCAP];
   uint32_t dw[MAXD][32];
   uint32_t glab[32];
+  unsigned long long wq_code[WQ_CAP];
+  double wq_rho[WQ_CAP];
 };
+
+// move the warp's buffered worklist items to the stream's global worklist
+// (one atomic per flush)
+__device__ __forceinline__ void flush_wq(WarpScratch& ws, int& wq_n,
+                                         uint32_t* counter,
+                                         unsigned long long* dq_code,
+                                         double* dq_rho, int lane) {
+  __syncwarp();
+  unsigned base = 0;
+  if (lane == 0) base = atomicAdd(counter, (unsigned)wq_n);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int e = lane; e < wq_n; e += 32) {
+    dq_code[(size_t)base + e] = ws.wq_code[e];
+    dq_rho[(size_t)base + e] = ws.wq_rho[e];
+  }
+  __syncwarp();
+  wq_n = 0;
+}
 
 __host__ __device__ inline size_t step_smem_bytes(int d, int G) {
   return 256 * 8 + (size_t)2 * d * G * 8 +
@@ -632,7 +721,6 @@ template <typename T, int KMAX>
 __global__ void __launch_bounds__(STEP_THREADS, 3)
     step_kernel(const StepArgs a) {
   extern __shared__ double s_mem[];
-  __shared__ int s_last;
   const int s = blockIdx.y;
   const int d = a.g.depth, G = a.g.n_groups;
   const int H = a.g.height, W = a.g.width, stride = a.g.stride;
@@ -677,6 +765,10 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
   const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
                   a.q.variance_floor, a.q.initial_variance};
   unsigned long long fg_count = 0;
+  const size_t dq_cap = dq_capacity(d, P);
+  unsigned long long* dq_code = (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
+  double* dq_rho = a.s.deeprho + (size_t)s * dq_cap;
+  int wq_n = 0;
 
   for (;;) {
     int wt = 0;
@@ -702,7 +794,7 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
         wc = a.q.weights[3 * cl + 2];
       }
       const bool member = valid && G > 0 && gid != (int)UNGROUPED;
-      unsigned lbits = 0, copybits = 0, gmmbits = 0;
+      unsigned lbits = 0, copybits = 0, gmmbits = 0, latebits = 0;
       int nq = 0;
       ws.glab[lane] = 0u;
 
@@ -718,21 +810,24 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
         o.rho = 0.0;
         o.rsel = 0;
         o.dyn = 0;
-        int vb = 0;
+        Pre<T> pre;
+        pre.vb = 0;
         if (valid) {
-          vb = frame[(size_t)c * P + p];
           if (do_reset) cold_reset<T, KMAX>(pr, p, a.q.initial_variance);
           if (do_reorder)
             cold_reorder<T>(pr, p, member ? s_gmu[c * G + gid]
                                           : (G > 0 ? s_gmu[c * G] : 0.0));
+          preload<T>(pr, p, frame + (size_t)c * P, f.grouping, member,
+                     f.sampling, f.compat, on_lat, a.q.chp_epsilon, pre);
           GroupConst gc;
           gc.ok = member;
           gc.mu = member ? s_gmu[c * G + gid] : 0.0;
           gc.thr = member ? s_gthr[c * G + gid] : 0.0;
-          hot_px<T>(a, f, pr, p, vb, on_lat, s_bt, wa, wb, wc, gc, o);
+          hot_px<T>(a, f, pr, p, pre, on_lat, s_bt, wa, wb, wc, gc, o);
           st(confo + (size_t)c * P + p, o.conf);
           kindo[(size_t)c * P + p] = (uint8_t)o.kind;
         }
+        const int vb = pre.vb;
         lbits |= ((unsigned)o.label & 1u) << c;
         if (o.kind == K_COPY && valid) {
           copybits |= 1u << c;
@@ -744,23 +839,49 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
           gmmbits |= 1u << c;
           ws.dw[c][lane] = o.dyn;
         }
-        // enqueue deep work
+        // deep work: in-warp when this plane has copy pixels (their anchors
+        // need final labels now), else onto the stream's global worklist
         const bool dq = valid && o.deep != DEEP_NONE;
         const unsigned qm = __ballot_sync(FULL, dq);
-        if (dq) {
-          const int pos = nq + __popc(qm & ((1u << lane) - 1u));
-          ws.qcode[pos] = (uint32_t)lane | ((uint32_t)c << 5) |
-                          ((uint32_t)o.deep << 7) | ((uint32_t)o.rsel << 9) |
-                          ((uint32_t)vb << 12);
-          ws.qrho[pos] = o.rho;
+        const bool inline_plane =
+            __ballot_sync(FULL, valid && o.kind == K_COPY) != 0u;
+        if (qm && inline_plane) {
+          if (dq) {
+            const int pos = nq + __popc(qm & ((1u << lane) - 1u));
+            ws.qcode[pos] = (uint32_t)lane | ((uint32_t)c << 5) |
+                            ((uint32_t)o.deep << 7) | ((uint32_t)o.rsel << 9) |
+                            ((uint32_t)vb << 12);
+            ws.qrho[pos] = o.rho;
+          }
+          nq += __popc(qm);
+        } else if (qm) {
+          if (wq_n + __popc(qm) > WQ_CAP)
+            flush_wq(ws, wq_n, sync + 3, dq_code, dq_rho, lane);
+          if (dq) {
+            const int pos = wq_n + __popc(qm & ((1u << lane) - 1u));
+            ws.wq_code[pos] = 1ull | ((unsigned long long)o.deep << 1) |
+                              ((unsigned long long)o.rsel << 3) |
+                              ((unsigned long long)c << 6) |
+                              ((unsigned long long)vb << 8) |
+                              ((unsigned long long)p << 16);
+            ws.wq_rho[pos] = o.rho;
+            gmmbits &= ~((unsigned)labeled_later << c);  // label patched later
+            if (labeled_later) latebits |= 1u << c;
+          }
+          wq_n += __popc(qm);
         }
-        nq += __popc(qm);
 
         // ---- per-plane reductions (label-independent)
+#ifndef COG_EXP_NOKINDS
         const unsigned peers = __match_any_sync(FULL, valid ? o.kind : 15);
         if (valid && lane == __ffs(peers) - 1)
           wacc[acc_kind(c, o.kind)] += (unsigned long long)__popc(peers);
+#endif
+#ifdef COG_EXP_NOGROUPRED
+        unsigned todo = 0;
+#else
         unsigned todo = __ballot_sync(FULL, member);
+#endif
         while (todo) {
           const int leader = __ffs(todo) - 1;
           const int g = __shfl_sync(FULL, gid, leader);
@@ -801,6 +922,9 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
 
       // ---- 2. deep pass: queued plane-pixels, one per lane
       __syncwarp();
+#ifdef COG_EXP_NODEEP
+      nq = 0;
+#endif
       for (int e = lane; e < nq; e += 32) {
         const uint32_t code = ws.qcode[e];
         const int owner = code & 31, c = (code >> 5) & 3;
@@ -832,6 +956,10 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
           label = (int)((glab >> c) & 1u);
           a.s.dyn[((size_t)s * d + c) * P + p] =
               ws.dw[c][lane] | ((uint32_t)label << 8);
+        } else if ((latebits >> c) & 1u) {
+          // the deep kernel sets the label bit (and the mask) if foreground
+          label = 0;
+          a.s.dyn[((size_t)s * d + c) * P + p] = ws.dw[c][lane];
         }
         const int src = (it == 0) ? label : (int)((row0_lbl >> c) & 1u);
         const int al = __shfl_sync(FULL, src, col - col % stride);
@@ -848,9 +976,10 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
       __syncwarp();
     }
   }
+  if (wq_n) flush_wq(ws, wq_n, sync + 3, dq_code, dq_rho, lane);
   if (lane == 0) wacc[acc_fg(d)] += fg_count;
 
-  // ---- publish this CTA's partials; the last CTA of the stream finalizes
+  // ---- publish this CTA's partials (the deep kernel finalizes the frame)
   __syncthreads();
   unsigned long long* gacc =
       (unsigned long long*)a.s.accum + (size_t)s * words;
@@ -859,10 +988,106 @@ __global__ void __launch_bounds__(STEP_THREADS, 3)
     for (int w = 0; w < STEP_WARPS; ++w) v += s_acc_all[w * words + i];
     if (v) atomicAdd(gacc + i, v);
   }
+}
+
+// ---------------------------------------------------------------------------
+// deep kernel: the stream's worklist of MEANVAR hits and GMM fall-throughs,
+// one plane-pixel per thread (dense warps).  GMM labels are OR-ed into the
+// dyn word and the mask; a pixel turning foreground here is counted exactly
+// once (atomicOr on its mask word returns the previous byte).  The last CTA
+// of each stream finalizes the frame.
+// ---------------------------------------------------------------------------
+template <typename T, int KMAX>
+__global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
+  __shared__ int s_last;
+  __shared__ unsigned long long s_fg;
+  const int s = blockIdx.y;
+  const int d = a.g.depth;
+  const size_t P = (size_t)a.g.height * a.g.width;
+  uint32_t* sync = a.s.sync + (size_t)s * 4;
+  const size_t dq_cap = dq_capacity(d, P);
+  unsigned long long* dq_code = (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
+  const double* dq_rho = a.s.deeprho + (size_t)s * dq_cap;
+  const size_t n = *(volatile uint32_t*)(sync + 3);
+  const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
+                  a.q.variance_floor, a.q.initial_variance};
+  uint8_t* mask = a.mask + (size_t)s * P;
+  if (threadIdx.x == 0) s_fg = 0;
+  __syncthreads();
+  unsigned fg = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const unsigned long long code = dq_code[i];
+    if (!(code & 1ull)) continue;
+    dq_code[i] = 0ull;
+    const int kindq = (int)((code >> 1) & 3), rs = (int)((code >> 3) & 7);
+    const int c = (int)((code >> 6) & 3);
+    const double v = (double)((code >> 8) & 0xFF);
+    const size_t p = (size_t)(code >> 16);
+    const double rho = dq_rho[i];
+    const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+    // meta and every slot of the mixture in one round of loads
+    const uint32_t meta = pr.meta[p];
+    Mix<KMAX> x;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      x.mu[k] = 0.0;
+      x.var[k] = 1.0;
+      x.w[k] = 0.0;
+      if (k < a.g.k) {
+        x.mu[k] = ldrw(pr.mu + k * P + p);
+        x.var[k] = ldrw(pr.var + k * P + p);
+        x.w[k] = ldrw(pr.w + k * P + p);
+      }
+    }
+    int n = meta_count(meta);
+    int inv[KMAX];
+    if (kindq == DEEP_MEANVAR) {
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k == rs) {
+          const double mm = (1.0 - rho) * x.mu[k] + rho * v;
+          x.mu[k] = mm;
+          const double dd = v - mm;
+          double s2 = (1.0 - rho) * x.var[k] + rho * (dd * dd);
+          if (s2 < a.q.variance_floor) s2 = a.q.variance_floor;
+          x.var[k] = s2;
+        }
+      }
+      sort_modes<KMAX>(x, n, inv);
+      store_mix_r<T, KMAX>(pr, p, n, x);
+      pr.meta[p] = (uint16_t)meta_with_refs(
+          meta, select_inv<KMAX>(inv, meta_ref(meta, 0)),
+          select_inv<KMAX>(inv, meta_ref(meta, 1)));
+    } else {
+      const int lbl = gmm_step<KMAX>(x, n, a.g.k, v, rho, gp, inv);
+      store_mix_r<T, KMAX>(pr, p, n, x);
+      uint32_t nm = meta_with_count(meta, n);
+      if (kindq == DEEP_GMM)
+        nm = meta_with_refs(nm, select_inv<KMAX>(inv, meta_ref(meta, 0)),
+                            select_inv<KMAX>(inv, meta_ref(meta, 1)));
+      pr.meta[p] = (uint16_t)nm;
+      if (lbl) {
+        pr.dyn[p] |= 1u << 8;
+        const uintptr_t addr = (uintptr_t)(mask + p);
+        unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
+        const unsigned sh = (unsigned)(addr & 3) * 8;
+        const unsigned old = atomicOr(word, 0xFFu << sh);
+        fg += ((old >> sh) & 0xFFu) == 0u;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) fg += __shfl_xor_sync(FULL, fg, o);
+  if ((threadIdx.x & 31) == 0 && fg) atomicAdd(&s_fg, (unsigned long long)fg);
+  __syncthreads();
+  const int words = acc_words(d, a.g.n_groups);
+  unsigned long long* gacc =
+      (unsigned long long*)a.s.accum + (size_t)s * words;
+  if (threadIdx.x == 0 && s_fg) atomicAdd(gacc + acc_fg(d), s_fg);
   if (!a.fuse_finalize) return;
   __threadfence();
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     const unsigned t = atomicAdd(sync, 1u);
     s_last = (t == gridDim.x - 1);
   }
@@ -1314,6 +1539,13 @@ StepFn<T> pick_baseline(int K) {
 }
 
 template <typename T>
+StepFn<T> pick_deep(int K) {
+  if (K <= 3) return deep_kernel<T, 3>;
+  if (K <= 5) return deep_kernel<T, 5>;
+  return deep_kernel<T, 8>;
+}
+
+template <typename T>
 int launch_step(const StepArgs& a, cudaStream_t st) {
   auto fn = pick_step<T>(a.g.k);
   const size_t smem = step_smem_bytes(a.g.depth, a.g.n_groups);
@@ -1328,8 +1560,16 @@ int launch_step(const StepArgs& a, cudaStream_t st) {
   int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
   int gx = need < per_stream ? need : per_stream;
   if (gx < 1) gx = 1;
-  dim3 grid(gx, a.g.streams);
-  fn<<<grid, STEP_THREADS, smem, st>>>(a);
+  fn<<<dim3(gx, a.g.streams), STEP_THREADS, smem, st>>>(a);
+  int rc = launch_status();
+  if (rc) return rc;
+  // deep pass: fixed persistent grid (the worklist length is on the device)
+  const size_t P = (size_t)a.g.height * a.g.width;
+  size_t dg = (P * a.g.depth / 8 + 255) / 256;  // covers ~12% deep items
+  const size_t cap = (size_t)num_sms() * 8 / a.g.streams + 1;
+  if (dg > cap) dg = cap;
+  if (dg < 1) dg = 1;
+  pick_deep<T>(a.g.k)<<<dim3((unsigned)dg, a.g.streams), 256, 0, st>>>(a);
   return launch_status();
 }
 
@@ -1346,6 +1586,10 @@ const char* cog_version(void) {
 
 int64_t cog_accum_words(int32_t depth, int32_t n_groups) {
   return acc_words(depth, n_groups);
+}
+
+int64_t cog_deepq_slots(int32_t depth, int64_t n_pix) {
+  return (int64_t)dq_capacity(depth, (size_t)n_pix);
 }
 
 int cog_prior_build(const uint8_t* frames, int32_t n_frames, int32_t depth,

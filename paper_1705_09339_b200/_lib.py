@@ -121,6 +121,7 @@ _SIGS = {
     "cog_export_state": (ctypes.c_int, [_P, _P, _P, _P]),
     "cog_import_state": (ctypes.c_int, [_P, _P, _P, _P]),
     "cog_version": (ctypes.c_char_p, []),
+    "cog_debug_prof": (ctypes.c_int, [_P, ctypes.c_int]),
 }
 
 EXPORTED = tuple(_SIGS)

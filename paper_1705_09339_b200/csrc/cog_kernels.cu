@@ -33,6 +33,7 @@
 #include "../../include/cog_b200.h"
 
 #include <cstdio>
+#include <cstdlib>
 
 using namespace cog;
 
@@ -344,7 +345,7 @@ struct Pre {
   int vb;
   uint32_t dyn, meta, streak;
   float peak, tv;
-  T mut, vart;
+  T mu0, var0, mu1, var1;  // the MEAN (ref0) and MEANVAR (ref1) modes
 };
 
 // the mode slot whose (mu, var) the confidence reads, or -1 for the group
@@ -370,28 +371,82 @@ __device__ __forceinline__ bool will_evaluate(bool sampling, uint32_t dyn,
 }
 
 template <typename T>
-__device__ __forceinline__ void preload(const PlaneRef<T>& pr, size_t p,
-                                        const uint8_t* frame_c, bool grouping,
-                                        bool group_ok, bool sampling,
-                                        bool compat, bool on_lattice,
-                                        double eps, Pre<T>& x) {
+__device__ __forceinline__ void preload_r1(const PlaneRef<T>& pr, size_t p,
+                                           const uint8_t* frame_c, Pre<T>& x) {
   x.vb = frame_c[p];
   x.dyn = pr.dyn[p];
-  const bool evaluate =
-      !compat && will_evaluate(sampling, x.dyn, x.vb, on_lattice, eps);
   x.meta = pr.meta[p];
   x.streak = pr.streak[p];
   x.peak = __ldg(pr.peak + p);
+}
+
+template <typename T>
+__device__ __forceinline__ void preload_r2(const PlaneRef<T>& pr, size_t p,
+                                           bool sampling, bool compat,
+                                           bool on_lattice, double eps,
+                                           Pre<T>& x) {
   x.tv = 0.0f;
-  x.mut = (T)0;
-  x.vart = (T)1;
-  if (!evaluate) return;
-  x.tv = __ldg(pr.table + p * 256 + x.vb);
-  const int rt = top_ref(grouping, x.meta, group_ok);
-  if (rt >= 0) {
-    x.mut = pr.mu[(size_t)rt * pr.P + p];
-    x.vart = pr.var[(size_t)rt * pr.P + p];
+  x.mu0 = x.mu1 = (T)0;
+  x.var0 = x.var1 = (T)1;
+  if (compat || !will_evaluate(sampling, x.dyn, x.vb, on_lattice, eps)) return;
+  // one 32-B sector of a 1 KB row: bypass L1 (no 128-B line fill)
+#ifdef COG_EXP_NOTABLE
+  x.tv = 0.01f;
+#else
+  x.tv = __ldcg(pr.table + p * 256 + x.vb);
+#endif
+  const int r0 = meta_ref(x.meta, 0), r1 = meta_ref(x.meta, 1);
+  x.mu0 = pr.mu[(size_t)r0 * pr.P + p];
+  x.var0 = pr.var[(size_t)r0 * pr.P + p];
+  if (r1 != r0) {
+    x.mu1 = pr.mu[(size_t)r1 * pr.P + p];
+    x.var1 = pr.var[(size_t)r1 * pr.P + p];
+  } else {
+    x.mu1 = x.mu0;
+    x.var1 = x.var0;
   }
+}
+
+// ---------------------------------------------------------------------------
+// float32-state mode: confidence and level tests in fp32 with filtered
+// decisions.  Every comparison whose fp32 operands are within a relative
+// margin of each other (far above the fp32 error bound, ~1e-6) is redone in
+// binary64 exactly as the reference does; all decisions are therefore the
+// reference's, while continuous values (conf, rho) carry fp32 rounding.
+// ---------------------------------------------------------------------------
+constexpr float FILTER_MARGIN = 1e-5f;
+
+// reference form: |v - mu| <= lam * sqrt(var)
+__device__ __noinline__ bool match_exact(double v, double mu, double var,
+                                         double lam) {
+  return fabs(v - mu) <= lam * sqrt(var);
+}
+
+__device__ __forceinline__ bool match_filtered(float vf, float mu, float var,
+                                               float lamf, double lam) {
+  const float thr = lamf * sqrtf(var);
+  const float gap = fabsf(vf - mu) - thr;
+  if (gap < -FILTER_MARGIN * thr) return true;
+  if (gap > FILTER_MARGIN * thr) return false;
+  return match_exact((double)vf, (double)mu, (double)var, lam);
+}
+
+// reference confidence (kernels_numba.py:243-270), binary64
+__device__ __noinline__ double conf_exact(double v, double prev, double mu_top,
+                                          double den, double tv, double peak,
+                                          double wa, double wb, double wc,
+                                          double prior_floor, int literal) {
+  const double phat = tv / peak;
+  double bterm = fabs(v - prev) / 255.0;
+  if (!literal) bterm = 1.0 - bterm;
+  double gterm = fabs(v - mu_top) / den;
+  if (gterm > 1.0) gterm = 1.0;
+  if (!literal) gterm = 1.0 - gterm;
+  if (phat < prior_floor) {
+    const double dd = wb + wc;
+    return dd > 0.0 ? (wb * bterm + wc * gterm) / dd : 0.0;
+  }
+  return wa * phat + wb * bterm + wc * gterm;
 }
 
 template <typename T>
@@ -444,6 +499,23 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
   }
 
   const uint32_t meta = pre.meta;
+#ifdef COG_EXP_SKELETON
+  // timing ablation: same loads/stores, trivial arithmetic
+  {
+    const float cf = pre.tv / pre.peak + (float)pre.mu0 * 1e-9f +
+                     (float)pre.var1 * 1e-9f + (float)pre.mu1 * 1e-9f +
+                     (float)pre.var0 * 1e-9f;
+    pr.streak[p] = pre.streak + 1u;
+    atomicAdd(pr.hits + p, 1u);
+    o.kind = L_GROUP;
+    o.label = 0;
+    o.conf = (double)cf;
+    o.rho = 0.0;
+    o.dyn = pack_dyn(vb, 0, waking, L_GROUP, clock) ^ (meta & 1u);
+    pr.dyn[p] = o.dyn;
+    return;
+  }
+#endif
   if (f.compat) {
     // kind from the pre-update rank-0 mode; the full update is deep work
     const int n = meta_count(meta);
@@ -461,39 +533,77 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
     return;
   }
 
-  // ---- confidence from the pre-update state
+  // ---- evaluation, branch-minimal: every level test is computed, the
+  // active level is the first hit in mid_order (kernels_numba.py:239-342)
   const int r0 = meta_ref(meta, 0), r1 = meta_ref(meta, 1);
-  const int m0 = meta_mid(meta, 0), m1 = meta_mid(meta, 1),
-            m2 = meta_mid(meta, 2);
-  int top = m0;
-  if (top == L_GROUP && !f.grouping) top = m1;
-  double mu_top, den;
-  double mu0 = 0.0, thr0 = 0.0;
-  bool have0 = false;
-  if (top == L_GROUP && gc.ok) {
-    mu_top = gc.mu;
-    den = gc.thr;
-  } else {
-    const int r = (top == L_MEANVAR) ? r1 : r0;
-    mu_top = (double)pre.mut;
-    den = q.match_lambda * sqrt((double)pre.vart);
-    if (r == r0) {
-      mu0 = mu_top;
-      thr0 = den;
-      have0 = true;
-    }
-  }
-  const double phat = (double)pre.tv / (double)pre.peak;
-  const double bterm = s_bt[dv];
-  double gterm = fabs(v - mu_top) / den;
-  if (gterm > 1.0) gterm = 1.0;
-  if (!f.literal) gterm = 1.0 - gterm;
+  const int c0 = (meta >> 4) & 3, c1 = (meta >> 6) & 3, c2 = (meta >> 8) & 3;
+  int top = c0;  // raw codes: 0 = none, 1 group, 2 mean, 3 mean+var
+  if (top == L_GROUP && !f.grouping) top = c1;
+  const bool group_top = (top == L_GROUP && gc.ok);
+  const bool top1 = (top == L_MEANVAR);
   double conf;
-  if (phat < q.prior_floor) {
-    const double dd = wb + wc;
-    conf = dd > 0.0 ? (wb * bterm + wc * gterm) / dd : 0.0;
+  bool t0, t1;
+  if constexpr (sizeof(T) == 4) {
+    // fp32 values; every decision filtered to the binary64 one
+    const float vf = (float)vb;
+    const float lamf = (float)q.match_lambda;
+    // sqrt via MUFU.RSQ (~2 ulp): only feeds filtered decisions / fp32 conf
+    const float v0f = (float)pre.var0, v1f = (float)pre.var1;
+    const float s0 = v0f * rsqrtf(v0f), s1 = v1f * rsqrtf(v1f);
+    const float mt = group_top ? (float)gc.mu : (top1 ? (float)pre.mu1 : (float)pre.mu0);
+    const float dn = group_top ? (float)gc.thr : lamf * (top1 ? s1 : s0);
+    const float ph = __fdividef(pre.tv, pre.peak);
+    const float bt = (float)s_bt[dv];
+    float gt = fminf(__fdividef(fabsf(vf - mt), dn), 1.0f);
+    if (!f.literal) gt = 1.0f - gt;
+    const float pf = (float)q.prior_floor;
+    float cf;
+    if (ph < pf) {
+      const float dd = (float)(wb + wc);
+      cf = dd > 0.0f ? __fdividef((float)wb * bt + (float)wc * gt, dd) : 0.0f;
+    } else {
+      cf = (float)wa * ph + (float)wb * bt + (float)wc * gt;
+    }
+    const float ct = (float)q.confidence_threshold;
+    conf = (double)cf;
+    if (fabsf(ph - pf) <= FILTER_MARGIN * pf + 1e-30f ||
+        fabsf(cf - ct) <= FILTER_MARGIN) {
+      const double den =
+          group_top ? gc.thr
+                    : q.match_lambda * sqrt((double)(top1 ? pre.var1 : pre.var0));
+      conf = conf_exact(v, (double)chp,
+                        group_top ? gc.mu : (double)(top1 ? pre.mu1 : pre.mu0),
+                        den, (double)pre.tv, (double)pre.peak, wa, wb, wc,
+                        q.prior_floor, f.literal);
+    }
+    const float thr0 = lamf * s0, thr1 = lamf * s1;
+    const float g0 = fabsf(vf - (float)pre.mu0) - thr0;
+    const float g1 = fabsf(vf - (float)pre.mu1) - thr1;
+    t0 = g0 <= 0.0f;
+    t1 = g1 <= 0.0f;
+    if (fabsf(g0) <= FILTER_MARGIN * thr0)
+      t0 = match_exact(v, (double)pre.mu0, (double)pre.var0, q.match_lambda);
+    if (fabsf(g1) <= FILTER_MARGIN * thr1)
+      t1 = match_exact(v, (double)pre.mu1, (double)pre.var1, q.match_lambda);
   } else {
-    conf = wa * phat + wb * bterm + wc * gterm;
+    // binary64 throughout, the reference's operation order
+    const double thr0 = q.match_lambda * sqrt((double)pre.var0);
+    const double thr1 = (r1 == r0) ? thr0 : q.match_lambda * sqrt((double)pre.var1);
+    const double mu_top = group_top ? gc.mu : (double)(top1 ? pre.mu1 : pre.mu0);
+    const double den = group_top ? gc.thr : (top1 ? thr1 : thr0);
+    const double phat = (double)pre.tv / (double)pre.peak;
+    const double bterm = s_bt[dv];
+    double gterm = fabs(v - mu_top) / den;
+    if (gterm > 1.0) gterm = 1.0;
+    if (!f.literal) gterm = 1.0 - gterm;
+    if (phat < q.prior_floor) {
+      const double dd = wb + wc;
+      conf = dd > 0.0 ? (wb * bterm + wc * gterm) / dd : 0.0;
+    } else {
+      conf = wa * phat + wb * bterm + wc * gterm;
+    }
+    t0 = fabs(v - (double)pre.mu0) <= thr0;
+    t1 = fabs(v - (double)pre.mu1) <= thr1;
   }
   double rho = q.learning_rate;
   if (f.rate) {
@@ -501,49 +611,37 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
     if (relax < q.rate_floor) relax = q.rate_floor;
     rho = q.learning_rate * relax;
   }
-
-  // ---- descend the cascade
+  const bool hitG = f.grouping && gc.ok && fabs(v - gc.mu) <= gc.thr;
   int active = -1;
   int label = 0;
   if (f.chp && !changed) {
     active = L_CHP;
     label = last_label;
   } else {
+    bool done = false;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const int code = j == 0 ? m0 : (j == 1 ? m1 : m2);
-      if (active >= 0 || code < 0) break;
-      if (code == L_GROUP) {
-        if (!f.grouping || !gc.ok) continue;
-        if (fabs(v - gc.mu) <= gc.thr) active = L_GROUP;
-      } else {
-        const int r = (code == L_MEAN) ? r0 : r1;
-        double mur, thr;
-        if (have0 && r == r0) {
-          mur = mu0;
-          thr = thr0;
-        } else {
-          mur = ldrw(pr.mu + (size_t)r * P + p);
-          thr = q.match_lambda * sqrt(ldrw(pr.var + (size_t)r * P + p));
-        }
-        if (fabs(v - mur) <= thr) {
-          double acc = 0.0;
-          for (int k = 0; k < r; ++k)
-            acc = acc + ldrw(pr.w + (size_t)k * P + p);
-          if (acc <= q.background_threshold) {
-            if (code == L_MEAN) {
-              active = L_MEAN;
-              st(pr.mu + (size_t)r * P + p, (1.0 - rho) * mur + rho * v);
-            } else {
-              active = L_MEANVAR;
-              o.deep = DEEP_MEANVAR;
-              o.rsel = r;
-            }
-          }
-        }
+      const int code = j == 0 ? c0 : (j == 1 ? c1 : c2);
+      if (!done && code == 0) done = true;
+      bool hit = (code == L_GROUP) ? hitG : (code == L_MEAN ? t0 : t1);
+      const int rr = (code == L_MEAN) ? r0 : r1;
+      if (!done && hit && code != L_GROUP && rr > 0) {
+        // a matched mode outside the background weight prefix is not a hit
+        double acc = 0.0;
+        for (int k = 0; k < rr; ++k) acc = acc + ldrw(pr.w + (size_t)k * P + p);
+        hit = acc <= q.background_threshold;
+      }
+      if (!done && hit) {
+        active = code;
+        done = true;
       }
     }
-    if (active < 0) {
+    if (active == L_MEAN) {
+      st(pr.mu + (size_t)r0 * P + p, (1.0 - rho) * (double)pre.mu0 + rho * v);
+    } else if (active == L_MEANVAR) {
+      o.deep = DEEP_MEANVAR;
+      o.rsel = r1;
+    } else if (active < 0) {
       active = L_GMM;
       o.deep = DEEP_GMM;
     }
@@ -711,283 +809,724 @@ __device__ __forceinline__ void flush_wq(WarpScratch& ws, int& wq_n,
   wq_n = 0;
 }
 
-__host__ __device__ inline size_t step_smem_bytes(int d, int G) {
-  return 256 * 8 + (size_t)2 * d * G * 8 +
-         (size_t)STEP_WARPS * acc_words(d, G) * 8 +
-         (size_t)STEP_WARPS * sizeof(WarpScratch);
+// ---------------------------------------------------------------------------
+// Per-tile work shared by both step kernels.  `fill(c, pre)` provides plane
+// c's preloaded values (global loads or shared-memory stages).
+// ---------------------------------------------------------------------------
+#ifdef COG_PROF
+__device__ unsigned long long g_prof[16];
+#define PROF_T(v) const long long v = clock64()
+#define PROF_ADD(i, dt) if (lane == 0) atomicAdd(&g_prof[i], (unsigned long long)(dt))
+#else
+#define PROF_T(v)
+#define PROF_ADD(i, dt)
+#endif
+
+struct TileCtx {
+  int s, d, G, lane, it, ty, tx, col, stride, cw, W;
+  size_t P, p;
+  bool valid, on_lat, member;
+  int gid, cls;
+};
+
+struct StepShared {
+  const double* bt;
+  const double* gmu;
+  const double* gthr;
+  unsigned long long* wacc;
+  WarpScratch* ws;
+  uint32_t* lk;            // lane-private kind counts [d*7][32]
+  uint32_t* lg;            // lane-private group sums [d*G][4][32] (or null)
+  unsigned long long* lq;  // lane-private group conf sums [d*G][32]
+};
+
+// lane-private group partials only while they stay small
+constexpr int LANE_GROUP_SLOTS = 16;  // d * G
+
+__host__ __device__ inline size_t lane_acc_bytes(int d, int G) {
+  size_t b = (size_t)d * 7 * 32 * 4;
+  if (d * G <= LANE_GROUP_SLOTS) b += (size_t)d * G * 32 * (4 * 4 + 8);
+  return b;
 }
 
+template <typename T, int KMAX, typename Fill>
+__device__ __forceinline__ void tile_pass(const StepArgs& a, const Flags& f,
+                                          const TileCtx& t, const StepShared& sh,
+                                          unsigned& row0_lbl, int& wq_n,
+                                          unsigned long long& fg_count,
+                                          unsigned long long* dq_code,
+                                          double* dq_rho, uint32_t* sync,
+                                          Fill fill) {
+  const int s = t.s, d = t.d, G = t.G, lane = t.lane, it = t.it;
+  const size_t P = t.P, p = t.p;
+  const bool valid = t.valid, member = t.member;
+  const int gid = t.gid;
+  WarpScratch& ws = *sh.ws;
+  T* confo = (T*)a.conf + (size_t)s * d * P;
+  uint8_t* kindo = a.kind + (size_t)s * d * P;
+  const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
+                  a.q.variance_floor, a.q.initial_variance};
+  double wa = 0.0, wb = 0.0, wc = 0.0;
+  if (valid) {
+    wa = a.q.weights[3 * t.cls];
+    wb = a.q.weights[3 * t.cls + 1];
+    wc = a.q.weights[3 * t.cls + 2];
+  }
+  unsigned lbits = 0, copybits = 0, gmmbits = 0, latebits = 0;
+  int nq = 0;
+  ws.glab[lane] = 0u;
+#ifdef COG_PROF
+  const long long tp0 = clock64();
+#endif
+
+  // ---- 1. hot pass, plane by plane
+#pragma unroll 1
+  for (int c = 0; c < d; ++c) {
+    const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+    HotOut o;
+    o.kind = 0;
+    o.label = 0;
+    o.deep = DEEP_NONE;
+    o.conf = 0.0;
+    o.rho = 0.0;
+    o.rsel = 0;
+    o.dyn = 0;
+    Pre<T> pre;
+    fill(c, pre);
+    if (valid) {
+      GroupConst gc;
+      gc.ok = member;
+      gc.mu = member ? sh.gmu[c * G + gid] : 0.0;
+      gc.thr = member ? sh.gthr[c * G + gid] : 0.0;
+      hot_px<T>(a, f, pr, p, pre, t.on_lat, sh.bt, wa, wb, wc, gc, o);
+      st(confo + (size_t)c * P + p, o.conf);
+      kindo[(size_t)c * P + p] = (uint8_t)o.kind;
+    }
+    const int vb = pre.vb;
+    lbits |= ((unsigned)o.label & 1u) << c;
+    if (o.kind == K_COPY && valid) {
+      copybits |= 1u << c;
+      ws.dw[c][lane] = o.dyn;
+    }
+    const bool labeled_later = valid && (o.deep == DEEP_GMM ||
+                                         o.deep == DEEP_COMPAT);
+    if (labeled_later) {
+      gmmbits |= 1u << c;
+      ws.dw[c][lane] = o.dyn;
+    }
+    // deep work: in-warp when this plane has copy pixels (their anchors
+    // need final labels now), else onto the stream's global worklist
+    const bool dq = valid && o.deep != DEEP_NONE;
+    const unsigned qm = __ballot_sync(FULL, dq);
+    const bool inline_plane =
+        __ballot_sync(FULL, valid && o.kind == K_COPY) != 0u;
+    if (qm && inline_plane) {
+      if (dq) {
+        const int pos = nq + __popc(qm & ((1u << lane) - 1u));
+        ws.qcode[pos] = (uint32_t)lane | ((uint32_t)c << 5) |
+                        ((uint32_t)o.deep << 7) | ((uint32_t)o.rsel << 9) |
+                        ((uint32_t)vb << 12);
+        ws.qrho[pos] = o.rho;
+      }
+      nq += __popc(qm);
+    } else if (qm) {
+      if (wq_n + __popc(qm) > WQ_CAP)
+        flush_wq(ws, wq_n, sync + 3, dq_code, dq_rho, lane);
+      if (dq) {
+        const int pos = wq_n + __popc(qm & ((1u << lane) - 1u));
+        ws.wq_code[pos] = 1ull | ((unsigned long long)o.deep << 1) |
+                          ((unsigned long long)o.rsel << 3) |
+                          ((unsigned long long)c << 6) |
+                          ((unsigned long long)vb << 8) |
+                          ((unsigned long long)p << 16);
+        ws.wq_rho[pos] = o.rho;
+        gmmbits &= ~((unsigned)labeled_later << c);  // label patched later
+        if (labeled_later) latebits |= 1u << c;
+      }
+      wq_n += __popc(qm);
+    }
+
+    // ---- per-plane partial sums (label-independent), lane-private
+    if (valid) sh.lk[(c * 7 + o.kind) * 32 + lane] += 1u;
+    if (sh.lg) {
+      if (member) {
+        const int slot = c * G + gid;
+        uint32_t* e = sh.lg + slot * 4 * 32 + lane;
+        e[0] += (uint32_t)vb;   // sum v over all members
+        e[32] += 1u;            // member count
+        if (o.kind == L_GROUP) {
+          e[64] += 1u;          // hit count
+          e[96] += (uint32_t)vb;
+          const double cq = o.conf * 4503599627370496.0;  // 2^52
+          sh.lq[slot * 32 + lane] += cq > 0.0 ? (unsigned long long)cq : 0ull;
+        }
+      }
+      continue;
+    }
+    unsigned todo = __ballot_sync(FULL, member);
+    while (todo) {
+      const int leader = __ffs(todo) - 1;
+      const int g = __shfl_sync(FULL, gid, leader);
+      const bool mine = member && gid == g;
+      const unsigned mm = __ballot_sync(FULL, mine);
+      todo &= ~mm;
+      const unsigned sall = warp_sum_u32(mine ? (unsigned)vb : 0u);
+      const bool hit = mine && o.kind == L_GROUP;
+      const unsigned hm = __ballot_sync(FULL, hit);
+      unsigned sv = 0, q2 = 0, q1 = 0, q0 = 0;
+      if (hm) {
+        unsigned long long qv = 0;
+        if (hit) {
+          const double cq = o.conf * 4503599627370496.0;  // 2^52
+          qv = cq > 0.0 ? (unsigned long long)cq : 0ull;
+        }
+        sv = warp_sum_u32(hit ? (unsigned)vb : 0u);
+        q2 = warp_sum_u32((unsigned)(qv >> 40));
+        q1 = warp_sum_u32((unsigned)((qv >> 20) & 0xFFFFFu));
+        q0 = warp_sum_u32((unsigned)(qv & 0xFFFFFu));
+      }
+      if (lane == 0) {
+        unsigned long long* e = sh.wacc + acc_grp(d, G, c, g);
+        e[4] += sall;
+        e[5] += (unsigned long long)__popc(mm);
+        if (hm) {
+          const unsigned long long Q = ((unsigned long long)q2 << 40) +
+                                       ((unsigned long long)q1 << 20) +
+                                       (unsigned long long)q0;
+          e[0] += (unsigned long long)__popc(hm);
+          e[1] += sv;
+          e[2] += Q >> CONF_SPLIT;
+          e[3] += Q & ((1ull << CONF_SPLIT) - 1ull);
+        }
+      }
+    }
+  }
+
+  // ---- 2. in-warp deep pass (planes with copy pixels only)
+  __syncwarp();
+#ifdef COG_PROF
+  const long long tp1 = clock64();
+  if (lane == 0) atomicAdd(&g_prof[8], (unsigned long long)(tp1 - tp0));
+#endif
+  for (int e = lane; e < nq; e += 32) {
+    const uint32_t code = ws.qcode[e];
+    const int owner = code & 31, c = (code >> 5) & 3;
+    const int kindq = (code >> 7) & 3, rs = (code >> 9) & 7;
+    const double v = (double)((code >> 12) & 0xFF);
+    const int oidx = it * 32 + owner;
+    const int orow = oidx / t.cw, ocol = oidx - orow * t.cw;
+    const size_t op =
+        (size_t)(t.ty * t.stride + orow) * t.W + (t.tx * t.cw + ocol);
+    const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+    const uint32_t meta = pr.meta[op];
+    if (kindq == DEEP_MEANVAR) {
+      cold_meanvar<T, KMAX>(pr, op, meta, rs, v, ws.qrho[e],
+                            a.q.variance_floor);
+    } else {
+      const int lbl = cold_gmm<T, KMAX>(pr, op, meta, v, ws.qrho[e], gp,
+                                        a.g.k, kindq == DEEP_GMM);
+      if (lbl) atomicOr(&ws.glab[owner], 1u << c);
+    }
+  }
+  __syncwarp();
+
+  // ---- 3. finish: GMM labels, copy resolution, union mask
+  const unsigned glab = ws.glab[lane];
+  int fg = 0;
+#pragma unroll 1
+  for (int c = 0; c < d; ++c) {
+    int label = (int)((lbits >> c) & 1u);
+    if ((gmmbits >> c) & 1u) {
+      label = (int)((glab >> c) & 1u);
+      a.s.dyn[((size_t)s * d + c) * P + p] =
+          ws.dw[c][lane] | ((uint32_t)label << 8);
+    } else if ((latebits >> c) & 1u) {
+      // the deep kernel sets the label bit (and the mask) if foreground
+      label = 0;
+      a.s.dyn[((size_t)s * d + c) * P + p] = ws.dw[c][lane];
+    }
+    const int src = (it == 0) ? label : (int)((row0_lbl >> c) & 1u);
+    const int al = __shfl_sync(FULL, src, t.col - t.col % t.stride);
+    if ((copybits >> c) & 1u) {
+      label = al;
+      a.s.dyn[((size_t)s * d + c) * P + p] =
+          ws.dw[c][lane] | ((uint32_t)al << 8);
+    }
+    if (it == 0) row0_lbl |= ((unsigned)label & 1u) << c;
+    fg |= label;
+  }
+  if (valid) a.mask[(size_t)s * P + p] = fg ? 255 : 0;
+  fg_count += __popc(__ballot_sync(FULL, valid && fg));
+  __syncwarp();
+}
+
+// shared prologue: constant tables, group constants, partial slices
+struct StepSmem {
+  double* bt;
+  double* gmu;
+  double* gthr;
+  unsigned long long* acc_all;
+  WarpScratch* ws;
+  uint32_t* lane;        // lane-private partials, lane_bytes per warp
+  size_t lane_bytes;
+  unsigned char* extra;  // per-warp staging (pipelined kernel)
+};
+
+__device__ __forceinline__ StepShared step_shared(const StepSmem& m, int warp,
+                                                  int d, int G, int words) {
+  StepShared sh;
+  sh.bt = m.bt;
+  sh.gmu = m.gmu;
+  sh.gthr = m.gthr;
+  sh.wacc = m.acc_all + warp * words;
+  sh.ws = m.ws + warp;
+  uint32_t* base = (uint32_t*)((unsigned char*)m.lane + warp * m.lane_bytes);
+  sh.lk = base;
+  sh.lg = nullptr;
+  sh.lq = nullptr;
+  if (d * G <= LANE_GROUP_SLOTS && G > 0) {
+    sh.lg = base + d * 7 * 32;
+    sh.lq = (unsigned long long*)(sh.lg + d * G * 4 * 32);
+  }
+  return sh;
+}
+
+// fold the lane-private partials into the warp slice (end of kernel)
+__device__ __forceinline__ void fold_lane_partials(const StepShared& sh, int d,
+                                                   int G, int lane) {
+  __syncwarp();
+  for (int i = lane; i < d * 7; i += 32) {
+    unsigned long long t = 0;
+    for (int l = 0; l < 32; ++l) t += sh.lk[i * 32 + l];
+    sh.wacc[acc_kind(i / 7, i % 7)] += t;
+  }
+  if (sh.lg) {
+    for (int slot = lane; slot < d * G; slot += 32) {
+      unsigned long long sv = 0, cn = 0, hc = 0, hv = 0, cq = 0;
+      for (int l = 0; l < 32; ++l) {
+        const uint32_t* e = sh.lg + slot * 4 * 32 + l;
+        sv += e[0];
+        cn += e[32];
+        hc += e[64];
+        hv += e[96];
+        cq += sh.lq[slot * 32 + l];
+      }
+      unsigned long long* g = sh.wacc + acc_grp(d, G, slot / G, slot % G);
+      g[0] += hc;
+      g[1] += hv;
+      g[2] += cq >> CONF_SPLIT;
+      g[3] += cq & ((1ull << CONF_SPLIT) - 1ull);
+      g[4] += sv;
+      g[5] += cn;
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ StepSmem step_prologue(const StepArgs& a,
+                                                  const Flags& f, int warps,
+                                                  double* s_mem) {
+  const int s = blockIdx.y, d = a.g.depth, G = a.g.n_groups;
+  const int words = acc_words(d, G);
+  StepSmem m;
+  m.bt = s_mem;
+  m.gmu = s_mem + 256;
+  m.gthr = m.gmu + d * G;
+  m.acc_all = (unsigned long long*)(m.gthr + d * G);
+  m.ws = (WarpScratch*)(m.acc_all + warps * words);
+  m.lane = (uint32_t*)(m.ws + warps);
+  m.lane_bytes = lane_acc_bytes(d, G);
+  m.extra = (unsigned char*)m.lane + (size_t)warps * m.lane_bytes;
+  for (size_t i = threadIdx.x; i < (size_t)warps * m.lane_bytes / 4;
+       i += blockDim.x)
+    m.lane[i] = 0u;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    const double b = (double)i / 255.0;
+    m.bt[i] = f.literal ? b : 1.0 - b;
+  }
+  const double* gmu = a.s.g_mu + (size_t)s * d * G;
+  const double* gvar = a.s.g_var + (size_t)s * d * G;
+  for (int i = threadIdx.x; i < d * G; i += blockDim.x) {
+    m.gmu[i] = gmu[i];
+    m.gthr[i] = a.q.match_lambda * sqrt(gvar[i]);
+  }
+  for (int i = threadIdx.x; i < warps * words; i += blockDim.x)
+    m.acc_all[i] = 0ull;
+  __syncthreads();
+  return m;
+}
+
+__device__ __forceinline__ void step_publish(const StepArgs& a,
+                                             const StepSmem& m, int warps) {
+  const int s = blockIdx.y;
+  const int words = acc_words(a.g.depth, a.g.n_groups);
+  __syncthreads();
+  unsigned long long* gacc =
+      (unsigned long long*)a.s.accum + (size_t)s * words;
+  for (int i = threadIdx.x; i < words; i += blockDim.x) {
+    unsigned long long v = 0;
+    for (int w = 0; w < warps; ++w) v += m.acc_all[w * words + i];
+    if (v) atomicAdd(gacc + i, v);
+  }
+}
+
+#ifndef COG_STEP_MINB
+#define COG_STEP_MINB 2
+#endif
+
+// ---------------------------------------------------------------------------
+// general step kernel: any stride / geometry; plane state loaded from global
+// memory (the next plane's first round issued before the current plane).
+// ---------------------------------------------------------------------------
 template <typename T, int KMAX>
-__global__ void __launch_bounds__(STEP_THREADS, 3)
+__global__ void __launch_bounds__(STEP_THREADS, COG_STEP_MINB)
     step_kernel(const StepArgs a) {
   extern __shared__ double s_mem[];
+  const Flags f{a.q.sampling_on != 0, a.q.grouping_on != 0,
+                a.q.rate_scaling_on != 0, a.q.chp_on != 0,
+                a.q.literal_conf != 0, a.q.compat != 0};
+  const StepSmem m = step_prologue(a, f, STEP_WARPS, s_mem);
   const int s = blockIdx.y;
   const int d = a.g.depth, G = a.g.n_groups;
   const int H = a.g.height, W = a.g.width, stride = a.g.stride;
   const size_t P = (size_t)H * W;
   const int words = acc_words(d, G);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* s_bt = s_mem;                      // [256]
-  double* s_gmu = s_mem + 256;               // [d*G]
-  double* s_gthr = s_gmu + d * G;            // [d*G]
-  unsigned long long* s_acc_all =
-      (unsigned long long*)(s_gthr + d * G);  // [warps][words]
-  WarpScratch* s_ws = (WarpScratch*)(s_acc_all + STEP_WARPS * words);
-  unsigned long long* wacc = s_acc_all + warp * words;
-  WarpScratch& ws = s_ws[warp];
-
-  const Flags f{a.q.sampling_on != 0, a.q.grouping_on != 0,
-                a.q.rate_scaling_on != 0, a.q.chp_on != 0,
-                a.q.literal_conf != 0, a.q.compat != 0};
-  for (int i = tid; i < 256; i += blockDim.x) {
-    const double b = (double)i / 255.0;
-    s_bt[i] = f.literal ? b : 1.0 - b;
-  }
-  const double* gmu = a.s.g_mu + (size_t)s * d * G;
-  const double* gvar = a.s.g_var + (size_t)s * d * G;
-  for (int i = tid; i < d * G; i += blockDim.x) {
-    s_gmu[i] = gmu[i];
-    s_gthr[i] = a.q.match_lambda * sqrt(gvar[i]);
-  }
-  for (int i = tid; i < STEP_WARPS * words; i += blockDim.x) s_acc_all[i] = 0ull;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const StepShared sh = step_shared(m, warp, d, G, words);
   uint32_t* sync = a.s.sync + (size_t)s * 4;
   const bool do_reset = (*(volatile uint32_t*)(sync + 1) & 1u) != 0;
   const bool do_reorder = a.reorder_now != 0;
-  __syncthreads();
-
   const uint8_t* frame = a.frame + (size_t)s * d * P;
   const uint8_t* cls = a.s.cls + (size_t)s * P;
   const uint16_t* gidp = a.s.gid + (size_t)s * P;
-  uint8_t* mask = a.mask + (size_t)s * P;
-  T* confo = (T*)a.conf + (size_t)s * d * P;
-  uint8_t* kindo = a.kind + (size_t)s * d * P;
   const int cw = a.cw, npx = stride * cw;
-  const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
-                  a.q.variance_floor, a.q.initial_variance};
   unsigned long long fg_count = 0;
   const size_t dq_cap = dq_capacity(d, P);
   unsigned long long* dq_code = (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
   double* dq_rho = a.s.deeprho + (size_t)s * dq_cap;
   int wq_n = 0;
 
+  // tile indices from a per-stream counter, fetched one tile ahead
+  int next_wt = 0;
+  if (lane == 0) next_wt = (int)atomicAdd(sync + 2, 1u);
   for (;;) {
-    int wt = 0;
-    if (lane == 0) wt = (int)atomicAdd(sync + 2, 1u);
-    wt = __shfl_sync(FULL, wt, 0);
+    const int wt = __shfl_sync(FULL, next_wt, 0);
     if (wt >= a.n_tiles) break;
-    const int ty = wt / a.tiles_x, tx = wt - ty * a.tiles_x;
+    if (lane == 0) next_wt = (int)atomicAdd(sync + 2, 1u);
     unsigned row0_lbl = 0;
+    TileCtx t;
+    t.s = s; t.d = d; t.G = G; t.lane = lane; t.stride = stride;
+    t.cw = cw; t.W = W; t.P = P;
+    t.ty = wt / a.tiles_x;
+    t.tx = wt - t.ty * a.tiles_x;
     for (int it = 0; it < a.iters; ++it) {
       const int idx = it * 32 + lane;
-      const int r = idx / cw, col = idx - r * cw;
-      const int y = ty * stride + r, x = tx * cw + col;
-      const bool valid = (idx < npx) && (y < H) && (x < W);
-      const size_t p = valid ? (size_t)y * W + x : 0;
-      const bool on_lat = ((a.g.row0 + y) % stride == 0) && (x % stride == 0);
-      int gid = (int)UNGROUPED;
-      double wa = 0.0, wb = 0.0, wc = 0.0;
-      if (valid) {
-        gid = gidp[p];
-        const int cl = cls[p];
-        wa = a.q.weights[3 * cl];
-        wb = a.q.weights[3 * cl + 1];
-        wc = a.q.weights[3 * cl + 2];
+      const int r = idx / cw;
+      t.it = it;
+      t.col = idx - r * cw;
+      const int y = t.ty * stride + r, x = t.tx * cw + t.col;
+      t.valid = (idx < npx) && (y < H) && (x < W);
+      t.p = t.valid ? (size_t)y * W + x : 0;
+      t.on_lat = ((a.g.row0 + y) % stride == 0) && (x % stride == 0);
+      t.gid = (int)UNGROUPED;
+      t.cls = 0;
+      if (t.valid) {
+        t.gid = gidp[t.p];
+        t.cls = cls[t.p];
       }
-      const bool member = valid && G > 0 && gid != (int)UNGROUPED;
-      unsigned lbits = 0, copybits = 0, gmmbits = 0, latebits = 0;
-      int nq = 0;
-      ws.glab[lane] = 0u;
-
-      // ---- 1. hot pass, plane by plane
+      t.member = t.valid && G > 0 && t.gid != (int)UNGROUPED;
+      // pending illumination reset / scheduled reorder (rare)
+      if (t.valid && (do_reset || do_reorder)) {
 #pragma unroll 1
-      for (int c = 0; c < d; ++c) {
-        const PlaneRef<T> pr = plane_ref<T>(a, s, c);
-        HotOut o;
-        o.kind = 0;
-        o.label = 0;
-        o.deep = DEEP_NONE;
-        o.conf = 0.0;
-        o.rho = 0.0;
-        o.rsel = 0;
-        o.dyn = 0;
-        Pre<T> pre;
-        pre.vb = 0;
-        if (valid) {
-          if (do_reset) cold_reset<T, KMAX>(pr, p, a.q.initial_variance);
+        for (int c = 0; c < d; ++c) {
+          const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+          if (do_reset) cold_reset<T, KMAX>(pr, t.p, a.q.initial_variance);
           if (do_reorder)
-            cold_reorder<T>(pr, p, member ? s_gmu[c * G + gid]
-                                          : (G > 0 ? s_gmu[c * G] : 0.0));
-          preload<T>(pr, p, frame + (size_t)c * P, f.grouping, member,
-                     f.sampling, f.compat, on_lat, a.q.chp_epsilon, pre);
-          GroupConst gc;
-          gc.ok = member;
-          gc.mu = member ? s_gmu[c * G + gid] : 0.0;
-          gc.thr = member ? s_gthr[c * G + gid] : 0.0;
-          hot_px<T>(a, f, pr, p, pre, on_lat, s_bt, wa, wb, wc, gc, o);
-          st(confo + (size_t)c * P + p, o.conf);
-          kindo[(size_t)c * P + p] = (uint8_t)o.kind;
-        }
-        const int vb = pre.vb;
-        lbits |= ((unsigned)o.label & 1u) << c;
-        if (o.kind == K_COPY && valid) {
-          copybits |= 1u << c;
-          ws.dw[c][lane] = o.dyn;
-        }
-        const bool labeled_later = valid && (o.deep == DEEP_GMM ||
-                                             o.deep == DEEP_COMPAT);
-        if (labeled_later) {
-          gmmbits |= 1u << c;
-          ws.dw[c][lane] = o.dyn;
-        }
-        // deep work: in-warp when this plane has copy pixels (their anchors
-        // need final labels now), else onto the stream's global worklist
-        const bool dq = valid && o.deep != DEEP_NONE;
-        const unsigned qm = __ballot_sync(FULL, dq);
-        const bool inline_plane =
-            __ballot_sync(FULL, valid && o.kind == K_COPY) != 0u;
-        if (qm && inline_plane) {
-          if (dq) {
-            const int pos = nq + __popc(qm & ((1u << lane) - 1u));
-            ws.qcode[pos] = (uint32_t)lane | ((uint32_t)c << 5) |
-                            ((uint32_t)o.deep << 7) | ((uint32_t)o.rsel << 9) |
-                            ((uint32_t)vb << 12);
-            ws.qrho[pos] = o.rho;
-          }
-          nq += __popc(qm);
-        } else if (qm) {
-          if (wq_n + __popc(qm) > WQ_CAP)
-            flush_wq(ws, wq_n, sync + 3, dq_code, dq_rho, lane);
-          if (dq) {
-            const int pos = wq_n + __popc(qm & ((1u << lane) - 1u));
-            ws.wq_code[pos] = 1ull | ((unsigned long long)o.deep << 1) |
-                              ((unsigned long long)o.rsel << 3) |
-                              ((unsigned long long)c << 6) |
-                              ((unsigned long long)vb << 8) |
-                              ((unsigned long long)p << 16);
-            ws.wq_rho[pos] = o.rho;
-            gmmbits &= ~((unsigned)labeled_later << c);  // label patched later
-            if (labeled_later) latebits |= 1u << c;
-          }
-          wq_n += __popc(qm);
-        }
-
-        // ---- per-plane reductions (label-independent)
-#ifndef COG_EXP_NOKINDS
-        const unsigned peers = __match_any_sync(FULL, valid ? o.kind : 15);
-        if (valid && lane == __ffs(peers) - 1)
-          wacc[acc_kind(c, o.kind)] += (unsigned long long)__popc(peers);
-#endif
-#ifdef COG_EXP_NOGROUPRED
-        unsigned todo = 0;
-#else
-        unsigned todo = __ballot_sync(FULL, member);
-#endif
-        while (todo) {
-          const int leader = __ffs(todo) - 1;
-          const int g = __shfl_sync(FULL, gid, leader);
-          const bool mine = member && gid == g;
-          const unsigned mm = __ballot_sync(FULL, mine);
-          todo &= ~mm;
-          const unsigned sall = warp_sum_u32(mine ? (unsigned)vb : 0u);
-          const bool hit = mine && o.kind == L_GROUP;
-          const unsigned hm = __ballot_sync(FULL, hit);
-          unsigned sv = 0, q2 = 0, q1 = 0, q0 = 0;
-          if (hm) {
-            unsigned long long qv = 0;
-            if (hit) {
-              const double cq = o.conf * 4503599627370496.0;  // 2^52
-              qv = cq > 0.0 ? (unsigned long long)cq : 0ull;
-            }
-            sv = warp_sum_u32(hit ? (unsigned)vb : 0u);
-            q2 = warp_sum_u32((unsigned)(qv >> 40));
-            q1 = warp_sum_u32((unsigned)((qv >> 20) & 0xFFFFFu));
-            q0 = warp_sum_u32((unsigned)(qv & 0xFFFFFu));
-          }
-          if (lane == 0) {
-            unsigned long long* e = wacc + acc_grp(d, G, c, g);
-            e[4] += sall;
-            e[5] += (unsigned long long)__popc(mm);
-            if (hm) {
-              const unsigned long long Q = ((unsigned long long)q2 << 40) +
-                                           ((unsigned long long)q1 << 20) +
-                                           (unsigned long long)q0;
-              e[0] += (unsigned long long)__popc(hm);
-              e[1] += sv;
-              e[2] += Q >> CONF_SPLIT;
-              e[3] += Q & ((1ull << CONF_SPLIT) - 1ull);
-            }
-          }
+            cold_reorder<T>(pr, t.p, t.member ? m.gmu[c * G + t.gid]
+                                              : (G > 0 ? m.gmu[c * G] : 0.0));
         }
       }
-
-      // ---- 2. deep pass: queued plane-pixels, one per lane
-      __syncwarp();
-#ifdef COG_EXP_NODEEP
-      nq = 0;
-#endif
-      for (int e = lane; e < nq; e += 32) {
-        const uint32_t code = ws.qcode[e];
-        const int owner = code & 31, c = (code >> 5) & 3;
-        const int kindq = (code >> 7) & 3, rs = (code >> 9) & 7;
-        const double v = (double)((code >> 12) & 0xFF);
-        const int oidx = it * 32 + owner;
-        const int orow = oidx / cw, ocol = oidx - orow * cw;
-        const size_t op = (size_t)(ty * stride + orow) * W + (tx * cw + ocol);
-        const PlaneRef<T> pr = plane_ref<T>(a, s, c);
-        const uint32_t meta = pr.meta[op];
-        if (kindq == DEEP_MEANVAR) {
-          cold_meanvar<T, KMAX>(pr, op, meta, rs, v, ws.qrho[e],
-                                a.q.variance_floor);
-        } else {
-          const int lbl = cold_gmm<T, KMAX>(pr, op, meta, v, ws.qrho[e], gp,
-                                            a.g.k, kindq == DEEP_GMM);
-          if (lbl) atomicOr(&ws.glab[owner], 1u << c);
-        }
-      }
-      __syncwarp();
-
-      // ---- 3. finish: GMM labels, copy resolution, union mask
-      const unsigned glab = ws.glab[lane];
-      int fg = 0;
-#pragma unroll 1
-      for (int c = 0; c < d; ++c) {
-        int label = (int)((lbits >> c) & 1u);
-        if ((gmmbits >> c) & 1u) {
-          label = (int)((glab >> c) & 1u);
-          a.s.dyn[((size_t)s * d + c) * P + p] =
-              ws.dw[c][lane] | ((uint32_t)label << 8);
-        } else if ((latebits >> c) & 1u) {
-          // the deep kernel sets the label bit (and the mask) if foreground
-          label = 0;
-          a.s.dyn[((size_t)s * d + c) * P + p] = ws.dw[c][lane];
-        }
-        const int src = (it == 0) ? label : (int)((row0_lbl >> c) & 1u);
-        const int al = __shfl_sync(FULL, src, col - col % stride);
-        if ((copybits >> c) & 1u) {
-          label = al;
-          a.s.dyn[((size_t)s * d + c) * P + p] =
-              ws.dw[c][lane] | ((uint32_t)al << 8);
-        }
-        if (it == 0) row0_lbl |= ((unsigned)label & 1u) << c;
-        fg |= label;
-      }
-      if (valid) mask[p] = fg ? 255 : 0;
-      fg_count += __popc(__ballot_sync(FULL, valid && fg));
-      __syncwarp();
+      const size_t p = t.p;
+      const bool valid = t.valid, on_lat = t.on_lat;
+      // first-round loads of plane c+1 are issued before plane c is
+      // evaluated (the callback runs once per plane, in order)
+      Pre<T> nxt;
+      nxt.vb = 0;
+      nxt.dyn = nxt.meta = nxt.streak = 0u;
+      nxt.peak = 1.0f;
+      if (valid) preload_r1<T>(plane_ref<T>(a, s, 0), p, frame, nxt);
+      tile_pass<T, KMAX>(
+          a, f, t, sh, row0_lbl, wq_n, fg_count, dq_code, dq_rho, sync,
+          [&](int c, Pre<T>& pre) {
+            pre = nxt;
+            nxt.vb = 0;
+            nxt.dyn = nxt.meta = nxt.streak = 0u;
+            nxt.peak = 1.0f;
+            if (valid && c + 1 < d)
+              preload_r1<T>(plane_ref<T>(a, s, c + 1), p,
+                            frame + (size_t)(c + 1) * P, nxt);
+            pre.tv = 0.0f;
+            pre.mu0 = pre.mu1 = (T)0;
+            pre.var0 = pre.var1 = (T)1;
+            if (!valid) return;
+            preload_r2<T>(plane_ref<T>(a, s, c), p, f.sampling, f.compat,
+                          on_lat, a.q.chp_epsilon, pre);
+          });
     }
   }
-  if (wq_n) flush_wq(ws, wq_n, sync + 3, dq_code, dq_rho, lane);
-  if (lane == 0) wacc[acc_fg(d)] += fg_count;
+  if (wq_n) flush_wq(*sh.ws, wq_n, sync + 3, dq_code, dq_rho, lane);
+  fold_lane_partials(sh, d, G, lane);
+  if (lane == 0) sh.wacc[acc_fg(d)] += fg_count;
+  step_publish(a, m, STEP_WARPS);
+}
 
-  // ---- publish this CTA's partials (the deep kernel finalizes the frame)
-  __syncthreads();
-  unsigned long long* gacc =
-      (unsigned long long*)a.s.accum + (size_t)s * words;
-  for (int i = tid; i < words; i += blockDim.x) {
-    unsigned long long v = 0;
-    for (int w = 0; w < STEP_WARPS; ++w) v += s_acc_all[w * words + i];
-    if (v) atomicAdd(gacc + i, v);
+// ---------------------------------------------------------------------------
+// pipelined step kernel (strides 1/2/4, width % 4 == 0): each warp stages
+// the state of its upcoming tiles in shared memory with cp.async --
+// stage A (tile j+2): dyn, streak, peak, meta, frame bytes, class, group id
+// stage B (tile j+1, needs A): table entry at v and the two referenced
+//          modes' (mu, var), skipped for pixels the gate will not evaluate
+// compute (tile j) reads only shared memory; stores go straight to HBM.
+// Two tiles' loads are in flight behind every tile being evaluated.
+// ---------------------------------------------------------------------------
+constexpr int PIPE_WARPS = 4;
+constexpr int PIPE_THREADS = PIPE_WARPS * 32;
+
+__device__ __forceinline__ void cpa(void* dst, const void* src, int bytes,
+                                    bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa),
+                 "l"(src), "r"(pred ? 8 : 0)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa),
+                 "l"(src), "r"(pred ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cpa_wait2() {
+  asm volatile("cp.async.wait_group 2;" ::: "memory");
+}
+__device__ __forceinline__ void cpa_wait0() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+struct PipeLayout {  // byte offsets inside one warp's staging area
+  int a_dyn, a_streak, a_peak, a_meta, a_frame, a_cls, a_gid, a_bytes;
+  int b_tv, b_mu0, b_var0, b_mu1, b_var1, b_bytes;
+  int total;
+};
+
+__host__ __device__ inline PipeLayout pipe_layout(int d, int tsize) {
+  PipeLayout L;
+  L.a_dyn = 0;
+  L.a_streak = L.a_dyn + d * 128;
+  L.a_peak = L.a_streak + d * 128;
+  L.a_meta = L.a_peak + d * 128;
+  L.a_frame = L.a_meta + d * 64;
+  L.a_cls = L.a_frame + d * 32;
+  L.a_gid = L.a_cls + 32;
+  L.a_bytes = ((L.a_gid + 64) + 15) & ~15;
+  L.b_tv = 0;
+  L.b_mu0 = d * 128;
+  L.b_var0 = L.b_mu0 + d * 32 * tsize;
+  L.b_mu1 = L.b_var0 + d * 32 * tsize;
+  L.b_var1 = L.b_mu1 + d * 32 * tsize;
+  L.b_bytes = ((L.b_var1 + d * 32 * tsize) + 15) & ~15;
+  L.total = 3 * L.a_bytes + 2 * L.b_bytes;
+  return L;
+}
+
+#ifndef COG_PIPE_MINB
+#define COG_PIPE_MINB 4
+#endif
+
+template <typename T, int KMAX>
+__global__ void __launch_bounds__(PIPE_THREADS, COG_PIPE_MINB)
+    pipe_kernel(const StepArgs a) {
+  extern __shared__ double s_mem[];
+  const Flags f{a.q.sampling_on != 0, a.q.grouping_on != 0,
+                a.q.rate_scaling_on != 0, a.q.chp_on != 0,
+                a.q.literal_conf != 0, a.q.compat != 0};
+  const StepSmem m = step_prologue(a, f, PIPE_WARPS, s_mem);
+  const int s = blockIdx.y;
+  const int d = a.g.depth, G = a.g.n_groups;
+  const int H = a.g.height, W = a.g.width, stride = a.g.stride;
+  const size_t P = (size_t)H * W;
+  const int words = acc_words(d, G);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const StepShared sh = step_shared(m, warp, d, G, words);
+  const PipeLayout L = pipe_layout(d, (int)sizeof(T));
+  unsigned char* stage = m.extra + (size_t)warp * L.total;
+  unsigned char* bufA[3] = {stage, stage + L.a_bytes, stage + 2 * L.a_bytes};
+  unsigned char* bufB[2] = {stage + 3 * L.a_bytes,
+                            stage + 3 * L.a_bytes + L.b_bytes};
+  uint32_t* sync = a.s.sync + (size_t)s * 4;
+  const bool do_reset = (*(volatile uint32_t*)(sync + 1) & 1u) != 0;
+  const bool do_reorder = a.reorder_now != 0;
+  const uint8_t* frame = a.frame + (size_t)s * d * P;
+  const uint8_t* cls = a.s.cls + (size_t)s * P;
+  const uint16_t* gidp = a.s.gid + (size_t)s * P;
+  const int cw = a.cw;
+  const int lrow = lane / cw, lcol = lane - lrow * cw;
+  unsigned long long fg_count = 0;
+  const size_t dq_cap = dq_capacity(d, P);
+  unsigned long long* dq_code = (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
+  double* dq_rho = a.s.deeprho + (size_t)s * dq_cap;
+  int wq_n = 0;
+
+  // this lane's pixel of tile wt
+  auto pix = [&](int wt, size_t& p, bool& valid, bool& on_lat) {
+    const int ty = wt / a.tiles_x, tx = wt - ty * a.tiles_x;
+    const int y = ty * stride + lrow, x = tx * cw + lcol;
+    valid = wt < a.n_tiles && y < H && x < W;
+    p = valid ? (size_t)y * W + x : 0;
+    on_lat = ((a.g.row0 + y) % stride == 0) && (x % stride == 0);
+  };
+  auto cold = [&](int wt) {  // pending reset / reorder before staging
+    size_t p;
+    bool valid, on_lat;
+    pix(wt, p, valid, on_lat);
+    if (valid) {
+      const int gid = gidp[p];
+      const bool member = G > 0 && gid != (int)UNGROUPED;
+#pragma unroll 1
+      for (int c = 0; c < d; ++c) {
+        const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+        if (do_reset) cold_reset<T, KMAX>(pr, p, a.q.initial_variance);
+        if (do_reorder)
+          cold_reorder<T>(pr, p, member ? m.gmu[c * G + gid]
+                                        : (G > 0 ? m.gmu[c * G] : 0.0));
+      }
+    }
+    __syncwarp();
+  };
+  auto stage_a = [&](int wt, unsigned char* A) {
+    size_t p;
+    bool valid, on_lat;
+    pix(wt, p, valid, on_lat);
+    if (do_reset || do_reorder) cold(wt);
+#pragma unroll 1
+    for (int c = 0; c < d; ++c) {
+      const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+      cpa(A + L.a_dyn + c * 128 + lane * 4, pr.dyn + p, 4, valid);
+      cpa(A + L.a_streak + c * 128 + lane * 4, pr.streak + p, 4, valid);
+      cpa(A + L.a_peak + c * 128 + lane * 4, pr.peak + p, 4, valid);
+      if ((lane & 1) == 0)
+        cpa(A + L.a_meta + c * 64 + lane * 2, pr.meta + p, 4, valid);
+      if ((lane & 3) == 0)
+        cpa(A + L.a_frame + c * 32 + lane, frame + (size_t)c * P + p, 4,
+            valid);
+    }
+    if ((lane & 3) == 0) cpa(A + L.a_cls + lane, cls + p, 4, valid);
+    if ((lane & 1) == 0) cpa(A + L.a_gid + lane * 2, gidp + p, 4, valid);
+    cpa_commit();
+  };
+  auto stage_b = [&](int wt, const unsigned char* A, unsigned char* B) {
+    size_t p;
+    bool valid, on_lat;
+    pix(wt, p, valid, on_lat);
+#pragma unroll 1
+    for (int c = 0; c < d; ++c) {
+      const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+      const uint32_t dyn = ((const uint32_t*)(A + L.a_dyn + c * 128))[lane];
+      const uint32_t meta = ((const uint16_t*)(A + L.a_meta + c * 64))[lane];
+      const int vb = (A + L.a_frame + c * 32)[lane];
+      const bool ev = valid && !f.compat &&
+                      will_evaluate(f.sampling, dyn, vb, on_lat, a.q.chp_epsilon);
+      const int r0 = meta_ref(meta, 0), r1 = meta_ref(meta, 1);
+      cpa(B + L.b_tv + c * 128 + lane * 4, pr.table + p * 256 + vb, 4, ev);
+      cpa(B + L.b_mu0 + (c * 32 + lane) * sizeof(T), pr.mu + (size_t)r0 * P + p,
+          sizeof(T), ev);
+      cpa(B + L.b_var0 + (c * 32 + lane) * sizeof(T),
+          pr.var + (size_t)r0 * P + p, sizeof(T), ev);
+      cpa(B + L.b_mu1 + (c * 32 + lane) * sizeof(T), pr.mu + (size_t)r1 * P + p,
+          sizeof(T), ev);
+      cpa(B + L.b_var1 + (c * 32 + lane) * sizeof(T),
+          pr.var + (size_t)r1 * P + p, sizeof(T), ev);
+    }
+    cpa_commit();
+  };
+
+  // static round-robin tile assignment: tile j of this warp is gw + j*nw
+  const int nw = gridDim.x * PIPE_WARPS;
+  const int gw = blockIdx.x * PIPE_WARPS + warp;
+  int tj = gw, tj1 = gw + nw, tj2 = gw + 2 * nw;
+  stage_a(tj, bufA[0]);
+  stage_a(tj1, bufA[1]);
+  asm volatile("cp.async.wait_group 1;" ::: "memory");  // A(0) landed
+  __syncwarp();
+  stage_b(tj, bufA[0], bufB[0]);
+  for (int j = 0; tj < a.n_tiles; ++j) {
+    const int t3 = tj2 + nw;
+    PROF_T(c0);
+    stage_a(tj2, bufA[(j + 2) % 3]);
+    PROF_T(c1);
+    cpa_wait2();  // A(j+1) landed
+    __syncwarp();
+    PROF_T(c2);
+    stage_b(tj1, bufA[(j + 1) % 3], bufB[(j + 1) & 1]);
+    PROF_T(c3);
+    cpa_wait2();  // B(j) landed
+    __syncwarp();
+    PROF_T(c4);
+    PROF_ADD(0, c1 - c0);
+    PROF_ADD(1, c2 - c1);
+    PROF_ADD(2, c3 - c2);
+    PROF_ADD(3, c4 - c3);
+
+    // ---- evaluate tile j from shared memory
+    const unsigned char* A = bufA[j % 3];
+    const unsigned char* B = bufB[j & 1];
+    TileCtx t;
+    t.s = s; t.d = d; t.G = G; t.lane = lane; t.stride = stride;
+    t.cw = cw; t.W = W; t.P = P; t.it = 0;
+    t.ty = tj / a.tiles_x;
+    t.tx = tj - t.ty * a.tiles_x;
+    t.col = lcol;
+    pix(tj, t.p, t.valid, t.on_lat);
+    t.gid = ((const uint16_t*)(A + L.a_gid))[lane];
+    t.cls = (A + L.a_cls)[lane];
+    t.member = t.valid && G > 0 && t.gid != (int)UNGROUPED;
+    unsigned row0_lbl = 0;
+    tile_pass<T, KMAX>(
+        a, f, t, sh, row0_lbl, wq_n, fg_count, dq_code, dq_rho, sync,
+        [&](int c, Pre<T>& pre) {
+          pre.vb = (A + L.a_frame + c * 32)[lane];
+          pre.dyn = ((const uint32_t*)(A + L.a_dyn + c * 128))[lane];
+          pre.meta = ((const uint16_t*)(A + L.a_meta + c * 64))[lane];
+          pre.streak = ((const uint32_t*)(A + L.a_streak + c * 128))[lane];
+          pre.peak = ((const float*)(A + L.a_peak + c * 128))[lane];
+          pre.tv = ((const float*)(B + L.b_tv + c * 128))[lane];
+          pre.mu0 = ((const T*)(B + L.b_mu0))[c * 32 + lane];
+          pre.var0 = ((const T*)(B + L.b_var0))[c * 32 + lane];
+          pre.mu1 = ((const T*)(B + L.b_mu1))[c * 32 + lane];
+          pre.var1 = ((const T*)(B + L.b_var1))[c * 32 + lane];
+          if (!t.valid) {
+            pre.peak = 1.0f;
+            pre.var0 = pre.var1 = (T)1;
+          }
+        });
+    PROF_T(c5);
+    PROF_ADD(4, c5 - c4);
+    PROF_ADD(5, 1);
+    tj = tj1;
+    tj1 = tj2;
+    tj2 = t3;
   }
+  PROF_T(c6);
+  cpa_wait0();
+  if (wq_n) flush_wq(*sh.ws, wq_n, sync + 3, dq_code, dq_rho, lane);
+  fold_lane_partials(sh, d, G, lane);
+  if (lane == 0) sh.wacc[acc_fg(d)] += fg_count;
+  PROF_T(c7);
+  PROF_ADD(6, c7 - c6);
+  step_publish(a, m, PIPE_WARPS);
+  PROF_T(c8);
+  PROF_ADD(7, c8 - c7);
 }
 
 // ---------------------------------------------------------------------------
@@ -1474,6 +2013,20 @@ __global__ void import_kernel(cog_geom g, cog_state s, cog_ref_state in) {
 // ---------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------
+// Random 4-byte table lookups must not drag 64/128-B DRAM fetches along.
+void set_fetch_granularity() {
+  static bool done = false;
+  if (!done) {
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+    if (getenv("COG_DEBUG"))
+      fprintf(stderr, "cog: L2 fetch granularity -> %zu (rc %d)\n", got, (int)e);
+    cudaGetLastError();
+    done = true;
+  }
+}
+
 int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -1546,22 +2099,50 @@ StepFn<T> pick_deep(int K) {
 }
 
 template <typename T>
-int launch_step(const StepArgs& a, cudaStream_t st) {
-  auto fn = pick_step<T>(a.g.k);
-  const size_t smem = step_smem_bytes(a.g.depth, a.g.n_groups);
+StepFn<T> pick_pipe(int K) {
+  if (K <= 3) return pipe_kernel<T, 3>;
+  if (K <= 5) return pipe_kernel<T, 5>;
+  return pipe_kernel<T, 8>;
+}
+
+// the pipelined kernel needs one-pass warp tiles and 4-byte aligned rows
+bool pipe_ok(const StepArgs& a) {
+  if (getenv("COG_NO_PIPE")) return false;
+  const int st = a.g.stride;
+  return (st == 1 || st == 2 || st == 4) && a.iters == 1 &&
+         (a.g.width % 4) == 0 && ((uintptr_t)a.frame % 4) == 0;
+}
+
+template <typename T>
+int launch_hot(const StepArgs& a, cudaStream_t st) {
+  const bool pipe = pipe_ok(a);
+  auto fn = pipe ? pick_pipe<T>(a.g.k) : pick_step<T>(a.g.k);
+  const int threads = pipe ? PIPE_THREADS : STEP_THREADS;
+  const int warps = threads / 32;
+  size_t smem = 256 * 8 + (size_t)2 * a.g.depth * a.g.n_groups * 8 +
+                (size_t)warps * acc_words(a.g.depth, a.g.n_groups) * 8 +
+                (size_t)warps * sizeof(WarpScratch) +
+                (size_t)warps * lane_acc_bytes(a.g.depth, a.g.n_groups);
+  if (pipe) smem += (size_t)warps * pipe_layout(a.g.depth, sizeof(T)).total;
   if (smem > 200 * 1024) return COG_EUNSUPPORTED;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, STEP_THREADS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
   if (occ < 1) occ = 1;
-  const int need = (a.n_tiles + STEP_WARPS - 1) / STEP_WARPS;
+  const int need = (a.n_tiles + warps - 1) / warps;
   int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
   int gx = need < per_stream ? need : per_stream;
   if (gx < 1) gx = 1;
-  fn<<<dim3(gx, a.g.streams), STEP_THREADS, smem, st>>>(a);
-  int rc = launch_status();
+  fn<<<dim3(gx, a.g.streams), threads, smem, st>>>(a);
+  return launch_status();
+}
+
+template <typename T>
+int launch_step(const StepArgs& a, cudaStream_t st) {
+  set_fetch_granularity();
+  int rc = launch_hot<T>(a, st);
   if (rc) return rc;
   // deep pass: fixed persistent grid (the worklist length is on the device)
   const size_t P = (size_t)a.g.height * a.g.width;
@@ -1586,6 +2167,21 @@ const char* cog_version(void) {
 
 int64_t cog_accum_words(int32_t depth, int32_t n_groups) {
   return acc_words(depth, n_groups);
+}
+
+int cog_debug_prof(uint64_t* out16, int reset) {
+#ifdef COG_PROF
+  cudaMemcpyFromSymbol(out16, g_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+  }
+  return 0;
+#else
+  (void)out16;
+  (void)reset;
+  return COG_EUNSUPPORTED;
+#endif
 }
 
 int64_t cog_deepq_slots(int32_t depth, int64_t n_pix) {

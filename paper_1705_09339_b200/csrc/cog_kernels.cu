@@ -2010,6 +2010,8 @@ __global__ void import_kernel(cog_geom g, cog_state s, cog_ref_state in) {
   }
 }
 
+#include "cog_lean.cuh"
+
 // ---------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------
@@ -2105,9 +2107,56 @@ StepFn<T> pick_pipe(int K) {
   return pipe_kernel<T, 8>;
 }
 
+// step-kernel selection: COG_KERNEL=lean|pipe|general (default lean where
+// it applies; COG_NO_PIPE=1 forces the general kernel, for parity tests)
+int kernel_choice() {
+  const char* e = getenv("COG_KERNEL");
+  if (getenv("COG_NO_PIPE")) return 2;
+  if (!e) return 0;
+  if (e[0] == 'p') return 1;
+  if (e[0] == 'g') return 2;
+  return 0;
+}
+
+template <typename T>
+StepFn<T> pick_lean(int K, int d) {
+  if (d == 1) {
+    if (K <= 3) return lean_kernel<T, 3, 1>;
+    if (K <= 5) return lean_kernel<T, 5, 1>;
+    return lean_kernel<T, 8, 1>;
+  }
+  if (K <= 3) return lean_kernel<T, 3, 3>;
+  if (K <= 5) return lean_kernel<T, 5, 3>;
+  return lean_kernel<T, 8, 3>;
+}
+
+bool lean_ok(const StepArgs& a) {
+  return kernel_choice() == 0 && a.iters == 1 &&
+         (a.g.depth == 1 || a.g.depth == 3) && a.g.stride <= 5;
+}
+
+template <typename T>
+int launch_lean(const StepArgs& a, cudaStream_t st) {
+  auto fn = pick_lean<T>(a.g.k, a.g.depth);
+  const size_t smem = lean_smem_bytes(a.g.depth, a.g.n_groups);
+  if (smem > 200 * 1024) return COG_EUNSUPPORTED;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, LEAN_THREADS, smem);
+  if (occ < 1) occ = 1;
+  const int need = (a.n_tiles + LEAN_WARPS - 1) / LEAN_WARPS;
+  const int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
+  int gx = need < per_stream ? need : per_stream;
+  if (gx < 1) gx = 1;
+  fn<<<dim3(gx, a.g.streams), LEAN_THREADS, smem, st>>>(a);
+  return launch_status();
+}
+
 // the pipelined kernel needs one-pass warp tiles and 4-byte aligned rows
 bool pipe_ok(const StepArgs& a) {
-  if (getenv("COG_NO_PIPE")) return false;
+  if (kernel_choice() == 2) return false;
   const int st = a.g.stride;
   return (st == 1 || st == 2 || st == 4) && a.iters == 1 &&
          (a.g.width % 4) == 0 && ((uintptr_t)a.frame % 4) == 0;
@@ -2115,6 +2164,7 @@ bool pipe_ok(const StepArgs& a) {
 
 template <typename T>
 int launch_hot(const StepArgs& a, cudaStream_t st) {
+  if (lean_ok(a)) return launch_lean<T>(a, st);
   const bool pipe = pipe_ok(a);
   auto fn = pipe ? pick_pipe<T>(a.g.k) : pick_step<T>(a.g.k);
   const int threads = pipe ? PIPE_THREADS : STEP_THREADS;

@@ -295,6 +295,10 @@ class CascadeEngine:
         s = config.stride
         self.on_lattice = (((yy + row0) % s == 0) & (xx % s == 0)).astype(np.uint8)
         self.prior = None
+        self.row0 = row0
+        # row-band shard: callable summing the `accum` partials across the
+        # shards of one frame in place (parallel.py); None = whole frame
+        self.reducer = None
 
     # ------------------------------------------------------------ helpers
 
@@ -366,33 +370,8 @@ class CascadeEngine:
 
     def _export_arrays(self) -> dict:
         self.materialize()
-        d, P, K = self.depth, self.n_pix, self.config.k_max
-        dev = self.dev.device
-        bufs = {
-            "mu": torch.empty((d, P, K), dtype=torch.float64, device=dev),
-            "var": torch.empty((d, P, K), dtype=torch.float64, device=dev),
-            "w": torch.empty((d, P, K), dtype=torch.float64, device=dev),
-            "count": torch.empty((d, P), dtype=torch.int64, device=dev),
-            "mid_order": torch.empty((d, P, 3), dtype=torch.int8, device=dev),
-            "mode_ref": torch.empty((d, P, 2), dtype=torch.int8, device=dev),
-            "chp_prev": torch.empty((d, P), dtype=torch.uint8, device=dev),
-            "last_label": torch.empty((d, P), dtype=torch.uint8, device=dev),
-            "last_active": torch.empty((d, P), dtype=torch.int8, device=dev),
-            "waking": torch.empty((d, P), dtype=torch.uint8, device=dev),
-            "streak": torch.empty((d, P), dtype=torch.int64, device=dev),
-            "clock": torch.empty((d, P), dtype=torch.int64, device=dev),
-            "hits": torch.empty((d, P, 5), dtype=torch.int64, device=dev),
-        }
-        rs = _ref_struct(bufs)
-        rc = self.lib.cog_export_state(_lib.ref(self.dev.single_geom()),
-                                       _lib.ref(self.dev.stream_view(0)),
-                                       _lib.ref(rs), self.stream)
-        _lib.check(rc, "cog_export_state")
-        out = {k: v.cpu().numpy() for k, v in bufs.items()}
-        G = self.dev.n_groups
-        out["group_mu"] = self.dev.g_mu[0, :, :G].cpu().numpy().copy()
-        out["group_var"] = self.dev.g_var[0, :, :G].cpu().numpy().copy()
-        return out
+        return export_state(self.dev, 0, self.config.k_max, self.lib,
+                            self.stream)
 
     def _import_arrays(self, arrays: dict) -> None:
         d, P, K = self.depth, self.n_pix, self.config.k_max
@@ -434,6 +413,33 @@ class CascadeEngine:
 
     # ------------------------------------------------------------ runtime
 
+    def _launch_step(self, x: torch.Tensor, mask: torch.Tensor,
+                     stats: torch.Tensor) -> None:
+        """Enqueue one frame: ``cog_step`` with the frame tail fused into
+        the last CTA, or -- for a row-band shard (``self.reducer`` set) --
+        the step, the cross-shard sum of the exact partials, then
+        ``cog_finalize`` (identical on every shard)."""
+        banded = self.reducer is not None
+        geom, prm, st = (_lib.ref(self.dev.geom), _lib.ref(self._params()),
+                         _lib.ref(self.dev.cstate))
+        rc = self.lib.cog_step(
+            geom, prm, st, x.data_ptr(), mask.data_ptr(),
+            self.dev.conf.data_ptr(), self.dev.kind.data_ptr(),
+            stats.data_ptr(), self.frame_count, int(self._reorder_pending),
+            0 if banded else 1, self.stream)
+        _lib.check(rc, "cog_step")
+        if banded:
+            self.reducer(self.dev.accum)
+            rc = self.lib.cog_finalize(geom, prm, st, stats.data_ptr(),
+                                       self.frame_count, self.stream)
+            _lib.check(rc, "cog_finalize")
+        self._reorder_pending = False
+        cfg = self.config
+        self.frame_count += 1
+        if (not cfg.compat and cfg.reorder_interval > 0
+                and self.frame_count % cfg.reorder_interval == 0):
+            self._reorder_pending = True
+
     def process_frame(self, frame) -> tuple[LabelMask, FrameStats]:
         """One frame through the fused CUDA step (cascade.py:261-318)."""
         x = self._frame_tensor(frame)
@@ -442,19 +448,7 @@ class CascadeEngine:
         mask = torch.empty((self.height, self.width), dtype=torch.uint8,
                            device=dev)
         stats = torch.empty(16, dtype=torch.int64, device=dev)
-        rc = self.lib.cog_step(
-            _lib.ref(self.dev.geom), _lib.ref(self._params()),
-            _lib.ref(self.dev.cstate), x.data_ptr(), mask.data_ptr(),
-            self.dev.conf.data_ptr(), self.dev.kind.data_ptr(),
-            stats.data_ptr(), self.frame_count, int(self._reorder_pending), 1,
-            self.stream)
-        _lib.check(rc, "cog_step")
-        self._reorder_pending = False
-        cfg = self.config
-        self.frame_count += 1
-        if (not cfg.compat and cfg.reorder_interval > 0
-                and self.frame_count % cfg.reorder_interval == 0):
-            self._reorder_pending = True
+        self._launch_step(x, mask, stats)
         hm = torch.empty((self.height, self.width), dtype=torch.uint8,
                          pin_memory=True)
         hs = torch.empty(16, dtype=torch.int64, pin_memory=True)
@@ -472,19 +466,7 @@ class CascadeEngine:
         no synchronisation."""
         if self._host is not None:
             self._flush()
-        rc = self.lib.cog_step(
-            _lib.ref(self.dev.geom), _lib.ref(self._params()),
-            _lib.ref(self.dev.cstate), frame.data_ptr(), mask.data_ptr(),
-            self.dev.conf.data_ptr(), self.dev.kind.data_ptr(),
-            stats.data_ptr(), self.frame_count, int(self._reorder_pending), 1,
-            self.stream)
-        _lib.check(rc, "cog_step")
-        self._reorder_pending = False
-        cfg = self.config
-        self.frame_count += 1
-        if (not cfg.compat and cfg.reorder_interval > 0
-                and self.frame_count % cfg.reorder_interval == 0):
-            self._reorder_pending = True
+        self._launch_step(frame, mask, stats)
 
     def reorder_levels(self) -> None:
         """Re-sort the middle levels by hits, ties by prior mass; the hit
@@ -563,6 +545,56 @@ def _state_property(name):
 
 for _name in _STATE_FIELDS + _GROUP_FIELDS:
     setattr(CascadeEngine, _name, _state_property(_name))
+
+
+def export_state(dev: DeviceState, s: int, k: int, lib, stream) -> dict:
+    """Stream s of ``dev`` in the reference's dtypes and layouts
+    (cascade.py:143-158) via ``cog_export_state``; group modes (d, G)."""
+    d, P = dev.depth, dev.P
+    dv = dev.device
+    shapes = {
+        "mu": ((d, P, k), torch.float64), "var": ((d, P, k), torch.float64),
+        "w": ((d, P, k), torch.float64), "count": ((d, P), torch.int64),
+        "mid_order": ((d, P, 3), torch.int8),
+        "mode_ref": ((d, P, 2), torch.int8),
+        "chp_prev": ((d, P), torch.uint8), "last_label": ((d, P), torch.uint8),
+        "last_active": ((d, P), torch.int8), "waking": ((d, P), torch.uint8),
+        "streak": ((d, P), torch.int64), "clock": ((d, P), torch.int64),
+        "hits": ((d, P, 5), torch.int64)}
+    bufs = {n: torch.empty(sh, dtype=t, device=dv)
+            for n, (sh, t) in shapes.items()}
+    rs = _ref_struct(bufs)
+    rc = lib.cog_export_state(_lib.ref(dev.single_geom()),
+                              _lib.ref(dev.stream_view(s)), _lib.ref(rs),
+                              stream)
+    _lib.check(rc, "cog_export_state")
+    out = {n: b.cpu().numpy() for n, b in bufs.items()}
+    G = dev.n_groups
+    out["group_mu"] = dev.g_mu[s, :, :G].cpu().numpy().copy()
+    out["group_var"] = dev.g_var[s, :, :G].cpu().numpy().copy()
+    return out
+
+
+def frame_tensor(frame, depth: int, height: int, width: int,
+                 device) -> torch.Tensor:
+    """(d, H, W) uint8 CUDA tensor from a Frame, array or tensor, checked
+    against the model geometry (cascade.py:263-269 -> DataError)."""
+    if isinstance(frame, torch.Tensor):
+        t = frame if frame.dim() == 3 else frame.unsqueeze(0)
+    else:
+        if isinstance(frame, Frame):
+            arr = frame.stacked()
+        else:
+            arr = np.asarray(frame)
+        if arr.ndim == 2:
+            arr = arr[None]
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+    if tuple(t.shape) != (depth, height, width):
+        raise DataError(f"frame shape {tuple(t.shape)} != model "
+                        f"{(depth, height, width)}")
+    if t.dtype != torch.uint8:
+        raise DataError("frames must be uint8")
+    return t.to(device, non_blocking=True).contiguous()
 
 
 def _ref_struct(bufs: dict) -> "_lib.RefState":

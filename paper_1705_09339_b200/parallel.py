@@ -1,0 +1,393 @@
+"""Multi-stream and row-band execution of the CoG path.
+
+Two ways the per-pixel work shards, both with all state resident in HBM:
+
+* **Independent streams** (BASELINE C5: 64 streams of 1280x720): a
+  ``BatchEngine`` keeps S streams of one geometry in one set of buffers
+  (``cog_geom.streams = S``); one ``cog_step`` launch steps all of them and
+  every per-stream global (group update, illumination test, statistics)
+  stays on the device.  Across GPUs each rank owns ``streams_for_rank`` --
+  no collectives.
+
+* **One stream in row bands** (BASELINE C4: one 3840x2160 stream): each
+  shard is a ``CascadeEngine`` over rows [r0, r1) of the frame
+  (``cog_geom.row0 = r0``, ``total_pixels`` = the whole frame).  Band starts
+  are multiples of the sampling stride, so every copy pixel's anchor
+  ``(y - y % stride, x - x % stride)`` (kernels_numba.py:363-373) lies in
+  the same band and no halo is exchanged.  The two per-frame couplings of
+  the reference -- the group update (cascade.py:320-344) and the
+  illumination monitor (cascade.py:310-313) -- are whole-frame reductions:
+  each shard's step leaves its exact partial sums (integer counts, integer
+  intensity sums, 2^-52 fixed-point confidence sums) in ``accum``, a
+  reducer sums them across shards (one ~0.5 KB all-reduce), and
+  ``cog_finalize`` applies the identical update on every shard.  Because the
+  partials are exact integers, the sharded run equals the single-engine run
+  bit for bit.
+
+Training shards the same way, except the k-means grouping, which is global:
+each shard computes its band's behaviour features on the GPU, the features
+are gathered, every shard runs the (deterministic) host clustering on the
+whole frame and installs its band's slice of the group map.
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .cascade import (CascadeEngine, DeviceState, FrameStats, export_state,
+                      frame_tensor, params_from_config, weight_table)
+from .config import EngineConfig
+from .errors import DataError, TrainingError
+from .frame_io import LabelMask
+from .grouping import GroupMap, build_groups
+from .scene_prior import silverman_bandwidth, stack_training
+from .training import install_groups, train_device
+
+Gather = Callable[[np.ndarray, np.ndarray], tuple[np.ndarray, np.ndarray]]
+
+
+# ----------------------------------------------------------------- bands
+
+
+def band_rows(height: int, parts: int, stride: int) -> list[tuple[int, int]]:
+    """Split ``height`` rows into ``parts`` contiguous bands whose starts are
+    multiples of ``stride`` (as equal as the stride blocks allow)."""
+    if parts < 1 or stride < 1 or height < 1:
+        raise DataError("band_rows: height, parts and stride must be >= 1")
+    blocks = -(-height // stride)
+    if parts > blocks:
+        raise DataError(f"{height} rows (stride {stride}) cannot form "
+                        f"{parts} non-empty stride-aligned bands")
+    per, extra = divmod(blocks, parts)
+    out, b = [], 0
+    for i in range(parts):
+        nb = per + (1 if i < extra else 0)
+        r0, r1 = b * stride, min(height, (b + nb) * stride)
+        out.append((r0, r1))
+        b += nb
+    return out
+
+
+def streams_for_rank(n_streams: int, rank: int, world: int) -> list[int]:
+    """Contiguous block of stream indices owned by ``rank``."""
+    per, extra = divmod(n_streams, world)
+    start = rank * per + min(rank, extra)
+    return list(range(start, start + per + (1 if rank < extra else 0)))
+
+
+# -------------------------------------------------------------- reducers
+
+
+class DistReducer:
+    """Sums a shard's ``accum`` partials over a torch.distributed group
+    (NCCL on the GPU box, gloo in the CPU tests).  The words are u64 bit
+    patterns of non-negative sums stored in int64, so a two's-complement
+    integer all-reduce is exact."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def __call__(self, accum: torch.Tensor) -> None:
+        import torch.distributed as dist
+        dist.all_reduce(accum, op=dist.ReduceOp.SUM, group=self.group)
+
+
+def dist_gather_rows(group=None) -> Gather:
+    """Gather callable for ``train_band_engine``: all-gathers the per-band
+    feature rows of every rank (in rank = band order)."""
+    import torch.distributed as dist
+
+    def gather(feats: np.ndarray, w_final: np.ndarray):
+        world = dist.get_world_size(group)
+        n = torch.tensor([feats.shape[0]], dtype=torch.int64)
+        backend = dist.get_backend(group)
+        dev = torch.device("cuda", torch.cuda.current_device()) \
+            if backend == "nccl" else torch.device("cpu")
+        n = n.to(dev)
+        sizes = [torch.zeros_like(n) for _ in range(world)]
+        dist.all_gather(sizes, n, group=group)
+        sizes = [int(s.item()) for s in sizes]
+        m = max(sizes)
+        buf = torch.zeros((m, 3), dtype=torch.float64, device=dev)
+        buf[:feats.shape[0], :2] = torch.from_numpy(feats).to(dev)
+        buf[:feats.shape[0], 2] = torch.from_numpy(w_final).to(dev)
+        parts = [torch.zeros_like(buf) for _ in range(world)]
+        dist.all_gather(parts, buf, group=group)
+        full = torch.cat([q[:k] for q, k in zip(parts, sizes)]).cpu().numpy()
+        return np.ascontiguousarray(full[:, :2]), np.ascontiguousarray(full[:, 2])
+    return gather
+
+
+def band_group_map(groups: GroupMap, r0: int, r1: int, width: int) -> GroupMap:
+    """The band's slice of a whole-frame group map (group parameters are
+    global and shared by every band)."""
+    return GroupMap(groups.group_id[r0 * width:r1 * width].copy(), groups.mu,
+                    groups.var, groups.weight, groups.member_count)
+
+
+# ------------------------------------------------------ row-band training
+
+
+def train_band_engine(frames, config: EngineConfig, rows: tuple[int, int],
+                      gather: Gather | None = None, device=None,
+                      kde_windows=None) -> CascadeEngine:
+    """Train the shard of rows [r0, r1) of a stream.
+
+    ``frames``: the whole training sequence (list of Frame or (N, d, H, W)
+    uint8) -- only the band's rows go to the device; the whole frames stay
+    on the host for the global clustering.  ``gather(feats, w_final)``
+    returns the whole frame's features in row order (identity when None,
+    i.e. a single band covering the frame)."""
+    config.validate()
+    arr = stack_training(frames)
+    n, d, h, w = arr.shape
+    r0, r1 = rows
+    if not (0 <= r0 < r1 <= h) or r0 % config.stride:
+        raise DataError(f"band rows {rows} must be stride-aligned inside "
+                        f"0..{h}")
+    bw = silverman_bandwidth(arr) if config.kde_auto_bandwidth \
+        else float(config.kde_bandwidth)
+    eng = CascadeEngine(config, r1 - r0, w, d, device=device, row0=r0,
+                        total_pixels=h * w)
+    band = np.ascontiguousarray(arr[:, :, r0:r1, :].reshape(n, d, -1))
+    values = torch.from_numpy(band).to(eng.dev.device)
+    eng.prior, feats, w_final = train_device(eng, values, config, bw,
+                                             kde_windows)
+    flat = np.ascontiguousarray(arr.reshape(n, d, h * w))
+    if config.grouping:
+        f_loc, w_loc = feats.cpu().numpy(), w_final.cpu().numpy()
+        f_all, w_all = gather(f_loc, w_loc) if gather else (f_loc, w_loc)
+        if f_all.shape[0] != h * w:
+            raise TrainingError(f"gathered features cover {f_all.shape[0]} "
+                                f"pixels, frame has {h * w}")
+        groups = build_groups(f_all, w_all, flat, config)
+    else:
+        groups = GroupMap.empty(h * w, d)
+    install_groups(eng, band_group_map(groups, r0, r1, w))
+    lib = _lib.load()
+    rc = lib.cog_set_levels(_lib.ref(eng.dev.geom), _lib.ref(eng.dev.cstate),
+                            torch.cuda.current_stream(eng.dev.device).cuda_stream)
+    _lib.check(rc, "cog_set_levels")
+    eng.bandwidth = bw
+    eng.sample_count = n
+    return eng
+
+
+class BandSet:
+    """All row bands of one stream in one process -- the single-GPU form of
+    the row-band decomposition (used by the parity tests and to run C4 on
+    fewer GPUs than bands).  Per frame: every band's step with the frame
+    tail deferred, one device-side sum of the partials, every band's
+    ``cog_finalize``.  No shard waits on another inside a kernel."""
+
+    def __init__(self, engines: Sequence[CascadeEngine]):
+        self.engines = list(engines)
+        if not self.engines:
+            raise DataError("BandSet needs at least one band")
+        e0 = self.engines[0]
+        self.width, self.depth = e0.width, e0.depth
+        self.height = sum(e.height for e in self.engines)
+        self.rows = [(e.row0, e.row0 + e.height) for e in self.engines]
+
+    @classmethod
+    def train(cls, frames, config: EngineConfig, parts: int, device=None,
+              kde_windows=None) -> "BandSet":
+        arr = stack_training(frames)
+        rows = band_rows(arr.shape[2], parts, config.stride)
+        # features of every band are needed before any band can cluster:
+        # train the device phase of all bands first, cluster once
+        engines = []
+        n, d, h, w = arr.shape
+        bw = silverman_bandwidth(arr) if config.kde_auto_bandwidth \
+            else float(config.kde_bandwidth)
+        feats, wfin = [], []
+        for r0, r1 in rows:
+            eng = CascadeEngine(config, r1 - r0, w, d, device=device,
+                                row0=r0, total_pixels=h * w)
+            band = np.ascontiguousarray(arr[:, :, r0:r1, :].reshape(n, d, -1))
+            values = torch.from_numpy(band).to(eng.dev.device)
+            eng.prior, f, wf = train_device(eng, values, config, bw,
+                                            kde_windows)
+            if config.grouping:
+                feats.append(f.cpu().numpy())
+                wfin.append(wf.cpu().numpy())
+            eng.bandwidth = bw
+            eng.sample_count = n
+            engines.append(eng)
+        flat = np.ascontiguousarray(arr.reshape(n, d, h * w))
+        groups = (build_groups(np.concatenate(feats), np.concatenate(wfin),
+                               flat, config)
+                  if config.grouping else GroupMap.empty(h * w, d))
+        lib = _lib.load()
+        for eng, (r0, r1) in zip(engines, rows):
+            install_groups(eng, band_group_map(groups, r0, r1, w))
+            rc = lib.cog_set_levels(
+                _lib.ref(eng.dev.geom), _lib.ref(eng.dev.cstate),
+                torch.cuda.current_stream(eng.dev.device).cuda_stream)
+            _lib.check(rc, "cog_set_levels")
+        return cls(engines)
+
+    def process_frame_device(self, frame: torch.Tensor, mask: torch.Tensor,
+                             stats: torch.Tensor) -> None:
+        """frame (d, H, W) u8, mask (H, W) u8, stats (16,) i64 -- CUDA."""
+        bands = []
+        for eng, (r0, r1) in zip(self.engines, self.rows):
+            eng._flush()
+            st = torch.empty(16, dtype=torch.int64, device=stats.device)
+            x = frame[:, r0:r1].contiguous()
+            m = mask[r0:r1]
+            geom, prm, cst = (_lib.ref(eng.dev.geom), _lib.ref(eng._params()),
+                              _lib.ref(eng.dev.cstate))
+            rc = eng.lib.cog_step(
+                geom, prm, cst, x.data_ptr(), m.data_ptr(),
+                eng.dev.conf.data_ptr(), eng.dev.kind.data_ptr(),
+                st.data_ptr(), eng.frame_count, int(eng._reorder_pending), 0,
+                eng.stream)
+            _lib.check(rc, "cog_step")
+            bands.append((eng, geom, prm, cst, x))
+        total = torch.stack([e.dev.accum for e in self.engines]).sum(dim=0)
+        for eng, geom, prm, cst, x in bands:
+            eng.dev.accum.copy_(total)
+            rc = eng.lib.cog_finalize(geom, prm, cst, stats.data_ptr(),
+                                      eng.frame_count, eng.stream)
+            _lib.check(rc, "cog_finalize")
+            eng._reorder_pending = False
+            cfg = eng.config
+            eng.frame_count += 1
+            if (not cfg.compat and cfg.reorder_interval > 0
+                    and eng.frame_count % cfg.reorder_interval == 0):
+                eng._reorder_pending = True
+
+    def process_frame(self, frame) -> tuple[LabelMask, FrameStats]:
+        dev = self.engines[0].dev.device
+        x = frame_tensor(frame, self.depth, self.height, self.width, dev)
+        mask = torch.empty((self.height, self.width), dtype=torch.uint8,
+                           device=dev)
+        stats = torch.empty(16, dtype=torch.int64, device=dev)
+        self.process_frame_device(x, mask, stats)
+        return LabelMask(mask.cpu().numpy()), FrameStats(*stats.cpu().tolist()[:10])
+
+    def state(self, name: str) -> np.ndarray:
+        """A whole-frame state array assembled from the bands (reference
+        layout: pixel axis = rows of every band in order)."""
+        parts = [getattr(e, name) for e in self.engines]
+        if name in ("group_mu", "group_var"):
+            return parts[0]
+        return np.concatenate(parts, axis=1)
+
+
+# --------------------------------------------------------- batch engine
+
+
+class BatchEngine:
+    """S independent streams of one geometry in one set of HBM buffers;
+    one launch steps every stream (no collectives, per-stream globals on
+    the device)."""
+
+    def __init__(self, config: EngineConfig, height: int, width: int,
+                 depth: int, streams: int, device=None):
+        config.validate()
+        self.config = config
+        self.height, self.width, self.depth = height, width, depth
+        self.streams = streams
+        self.n_pix = height * width
+        self.lib = _lib.load()
+        self.dev = DeviceState(config, height, width, depth, streams=streams,
+                               device=device)
+        self._wtab = weight_table(config)
+        self.frame_count = 0
+        self._reorder_pending = False
+        self.group_w: list[np.ndarray] = [np.zeros(0)] * streams
+
+    @property
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.dev.device).cuda_stream
+
+    def _params(self):
+        return params_from_config(self.config, self._wtab)
+
+    @classmethod
+    def train(cls, frames_per_stream: Sequence, config: EngineConfig,
+              device=None, kde_windows=None) -> "BatchEngine":
+        """frames_per_stream[s]: training frames of stream s (list of Frame
+        or (N, d, H, W) uint8)."""
+        first = stack_training(frames_per_stream[0])
+        n, d, h, w = first.shape
+        S = len(frames_per_stream)
+        eng = cls(config, h, w, d, S, device=device)
+        proxy = CascadeEngine.__new__(CascadeEngine)  # param/geom carrier
+        proxy.config, proxy.dev, proxy._wtab = config, eng.dev, eng._wtab
+        proxy.exact_group_sums = False
+        maps = []
+        for s in range(S):
+            arr = first if s == 0 else stack_training(frames_per_stream[s])
+            if arr.shape[1:] != (d, h, w):
+                raise DataError(f"stream {s} geometry {arr.shape[1:]} != "
+                                f"{(d, h, w)}")
+            bw = silverman_bandwidth(arr) if config.kde_auto_bandwidth \
+                else float(config.kde_bandwidth)
+            flat = np.ascontiguousarray(arr.reshape(arr.shape[0], d, h * w))
+            values = torch.from_numpy(flat).to(eng.dev.device)
+            _, feats, wf = train_device(proxy, values, config, bw,
+                                        kde_windows, stream=s)
+            maps.append(build_groups(feats.cpu().numpy(), wf.cpu().numpy(),
+                                     flat, config)
+                        if config.grouping else GroupMap.empty(h * w, d))
+            del values
+        g = max(m.group_count for m in maps)
+        eng.dev.set_groups(g)
+        for s, m in enumerate(maps):
+            proxy.group_w = np.zeros(0)
+            install_groups(proxy, m, stream=s, resize=False)
+            eng.group_w[s] = m.weight.copy()
+        rc = eng.lib.cog_set_levels(_lib.ref(eng.dev.geom),
+                                    _lib.ref(eng.dev.cstate), eng.stream)
+        _lib.check(rc, "cog_set_levels")
+        return eng
+
+    def process_frames_device(self, frames: torch.Tensor, masks: torch.Tensor,
+                              stats: torch.Tensor) -> None:
+        """frames (S, d, H, W) u8, masks (S, H, W) u8, stats (S, 16) i64."""
+        if tuple(frames.shape) != (self.streams, self.depth, self.height,
+                                   self.width) or frames.dtype != torch.uint8:
+            raise DataError(f"frames must be ({self.streams}, {self.depth}, "
+                            f"{self.height}, {self.width}) uint8")
+        rc = self.lib.cog_step(
+            _lib.ref(self.dev.geom), _lib.ref(self._params()),
+            _lib.ref(self.dev.cstate), frames.data_ptr(), masks.data_ptr(),
+            self.dev.conf.data_ptr(), self.dev.kind.data_ptr(),
+            stats.data_ptr(), self.frame_count, int(self._reorder_pending), 1,
+            self.stream)
+        _lib.check(rc, "cog_step")
+        self._reorder_pending = False
+        self.frame_count += 1
+        cfg = self.config
+        if (not cfg.compat and cfg.reorder_interval > 0
+                and self.frame_count % cfg.reorder_interval == 0):
+            self._reorder_pending = True
+
+    def process_frames(self, frames) -> tuple[np.ndarray, np.ndarray]:
+        """frames (S, d, H, W) uint8 (host or CUDA) -> masks (S, H, W) u8,
+        stats (S, 10) int64 rows (FrameStats layout)."""
+        x = torch.as_tensor(frames).to(self.dev.device).contiguous()
+        masks = torch.empty((self.streams, self.height, self.width),
+                            dtype=torch.uint8, device=self.dev.device)
+        stats = torch.empty((self.streams, 16), dtype=torch.int64,
+                            device=self.dev.device)
+        self.process_frames_device(x, masks, stats)
+        return masks.cpu().numpy(), stats[:, :10].cpu().numpy()
+
+    def export_stream(self, s: int) -> dict:
+        """Reference-layout state of stream s (after materialising any
+        pending reset / reorder of every stream)."""
+        rc = self.lib.cog_apply_pending(
+            _lib.ref(self.dev.geom), _lib.ref(self._params()),
+            _lib.ref(self.dev.cstate), int(self._reorder_pending), self.stream)
+        _lib.check(rc, "cog_apply_pending")
+        self._reorder_pending = False
+        return export_state(self.dev, s, self.config.k_max, self.lib,
+                            self.stream)

@@ -20,12 +20,17 @@ from .scene_prior import (DYN_DYNAMIC, DYN_OSCILLATING, DYN_STATIC_DRIFT,
                           stack_training)
 
 
-def install_groups(eng: CascadeEngine, groups: GroupMap, stream: int = 0) -> None:
-    """Upload a group map into stream `stream` of the engine's buffers."""
+def install_groups(eng: CascadeEngine, groups: GroupMap, stream: int = 0,
+                   resize: bool = True) -> None:
+    """Upload a group map into stream `stream` of the engine's buffers.
+    ``resize=False`` (multi-stream buffers sized for the largest map) keeps
+    the group arrays; unused group slots are never referenced by an id."""
     dev = eng.dev
     g = groups.group_count
-    if g != dev.n_groups:
+    if resize and g != dev.n_groups:
         dev.set_groups(g)
+    elif g > dev.n_groups:
+        raise ValueError(f"{g} groups do not fit {dev.n_groups} slots")
     gid = np.where(groups.group_id < 0, -1, groups.group_id).astype(np.int16)
     dev.gid[stream] = torch.from_numpy(gid).to(dev.device)
     if g:
@@ -37,6 +42,35 @@ def install_groups(eng: CascadeEngine, groups: GroupMap, stream: int = 0) -> Non
             groups.member_count.astype(np.int32)).to(dev.device)
     eng.group_w = groups.weight.copy()
     eng.group_members = groups.member_count.copy()
+
+
+def train_device(eng: CascadeEngine, values: torch.Tensor,
+                 config: EngineConfig, bandwidth: float, kde_windows=None,
+                 stream: int = 0):
+    """Phase 1 + warm-up of stream `stream` of ``eng`` from training frames
+    already on the device, values (N, d, P) uint8: scene prior straight into
+    the engine's table / peak / class buffers, then the mixture warm-up.
+    Returns the grouping features (P, 2) f64 and final weights (P,) f64 as
+    device tensors (None when grouping is off)."""
+    dev = eng.dev
+    n, d, p = values.shape
+    lib = _lib.load()
+    cuda_stream = torch.cuda.current_stream(dev.device).cuda_stream
+    prior = build_scene_prior_device(
+        values, config, windows=kde_windows, bandwidth=bandwidth,
+        out_tables=dev.table[stream], out_peak=dev.peak[stream],
+        out_classes=dev.cls[stream], height=dev.height, width=dev.width)
+    feats = w_final = None
+    if config.grouping:
+        feats = torch.empty((p, 2), dtype=torch.float64, device=dev.device)
+        w_final = torch.empty(p, dtype=torch.float64, device=dev.device)
+    rc = lib.cog_gmm_warmup(
+        _lib.ref(dev.single_geom()), _lib.ref(eng._params()),
+        _lib.ref(dev.stream_view(stream)), values.data_ptr(), n,
+        feats.data_ptr() if feats is not None else None,
+        w_final.data_ptr() if w_final is not None else None, cuda_stream)
+    _lib.check(rc, "cog_gmm_warmup")
+    return prior, feats, w_final
 
 
 def train_engine(frames, config: EngineConfig, kde_windows=None,
@@ -51,29 +85,19 @@ def train_engine(frames, config: EngineConfig, kde_windows=None,
         else float(config.kde_bandwidth)
     eng = CascadeEngine(config, h, w, d, device=device)
     dev = eng.dev
-    lib = _lib.load()
-    stream = torch.cuda.current_stream(dev.device).cuda_stream
     flat = np.ascontiguousarray(arr.reshape(n, d, p))
     values = torch.from_numpy(flat).to(dev.device)
-    eng.prior = build_scene_prior_device(
-        values, config, windows=kde_windows, bandwidth=bw,
-        out_tables=dev.table[0], out_peak=dev.peak[0], out_classes=dev.cls[0],
-        height=h, width=w)
-    feats = torch.empty((p, 2), dtype=torch.float64, device=dev.device)
-    w_final = torch.empty(p, dtype=torch.float64, device=dev.device)
-    rc = lib.cog_gmm_warmup(
-        _lib.ref(dev.single_geom()), _lib.ref(eng._params()),
-        _lib.ref(dev.stream_view(0)), values.data_ptr(), n,
-        feats.data_ptr() if config.grouping else None,
-        w_final.data_ptr() if config.grouping else None, stream)
-    _lib.check(rc, "cog_gmm_warmup")
+    eng.prior, feats, w_final = train_device(eng, values, config, bw,
+                                             kde_windows)
     if config.grouping:
         groups = build_groups(feats.cpu().numpy(), w_final.cpu().numpy(),
                               flat, config)
     else:
         groups = GroupMap.empty(p, d)
     install_groups(eng, groups)
-    rc = lib.cog_set_levels(_lib.ref(dev.geom), _lib.ref(dev.cstate), stream)
+    lib = _lib.load()
+    rc = lib.cog_set_levels(_lib.ref(dev.geom), _lib.ref(dev.cstate),
+                            torch.cuda.current_stream(dev.device).cuda_stream)
     _lib.check(rc, "cog_set_levels")
     eng.bandwidth = bw
     eng.sample_count = n

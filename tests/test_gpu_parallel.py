@@ -1,0 +1,114 @@
+"""Row-band and multi-stream execution on one GPU.
+
+Row bands: the frame's rows are split into stride-aligned shards, each a
+CascadeEngine with its own row0; per frame every shard steps with the frame
+tail deferred, the exact partials are summed, every shard finalizes.  The
+sharded run must equal the single-engine run bit for bit (masks, stats and
+every state array) -- the partials are exact integers -- and, in float64
+state, agree with the reference's goldens like the single engine does.
+
+Batch: S independent streams in one set of buffers, one launch per frame,
+must equal S separate engines bit for bit.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.golden_util import STATE, config_for, load_case
+
+pytestmark = pytest.mark.gpu
+
+BAND_CASES = ["mixed", "sampling", "sampling_stride3", "illum_grouped",
+              "c3small", "c5small"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _single(frames, n_train, cfg):
+    from paper_1705_09339_b200.training import train_engine
+    return train_engine(frames[:n_train], cfg)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("parts", [2, 3])
+@pytest.mark.parametrize("name", BAND_CASES)
+def test_row_bands_equal_single_engine(name, parts, dtype):
+    from paper_1705_09339_b200.parallel import BandSet
+    rec, overrides = load_case(name)
+    cfg = config_for(overrides, state_dtype=dtype)
+    frames = rec["frames"]
+    n_train = int(rec["n_train"])
+    ref = _single(frames, n_train, cfg)
+    bands = BandSet.train(frames[:n_train], cfg, parts)
+    assert len(bands.engines) == parts
+    for nm in ("group_id",):
+        got = np.concatenate([e.group_id for e in bands.engines])
+        assert np.array_equal(got, ref.group_id)
+    for t in range(frames.shape[0] - n_train):
+        f = frames[n_train + t]
+        m1, s1 = ref.process_frame(f)
+        m2, s2 = bands.process_frame(f)
+        assert np.array_equal(m1.labels, m2.labels), (name, t)
+        assert s1.as_row() == s2.as_row(), (name, t)
+    for nm in STATE:
+        assert np.array_equal(bands.state(nm), getattr(ref, nm)), nm
+
+
+def test_row_bands_match_reference_golden_f64():
+    """Sharded float64 run against the reference's own outputs."""
+    from paper_1705_09339_b200.parallel import BandSet
+    rec, overrides = load_case("mixed")
+    cfg = config_for(overrides, state_dtype="float64")
+    frames = rec["frames"]
+    n_train = int(rec["n_train"])
+    bands = BandSet.train(frames[:n_train], cfg, 4)
+    agree = total = 0
+    for t in range(frames.shape[0] - n_train):
+        m, st = bands.process_frame(frames[n_train + t])
+        agree += int((m.labels == rec["masks"][t]).sum())
+        total += m.labels.size
+        assert st.as_row()[0] == rec["stats"][t][0]
+    assert agree / total >= 0.99995
+    for nm in ("count", "mid_order", "mode_ref", "chp_prev", "clock", "waking"):
+        same = np.mean(bands.state(nm) == rec["final_" + nm])
+        assert same >= 0.999, nm
+
+
+def test_train_band_engine_full_frame_equals_train_engine():
+    from paper_1705_09339_b200.parallel import train_band_engine
+    rec, overrides = load_case("c3small")
+    cfg = config_for(overrides)
+    frames = rec["frames"]
+    n_train = int(rec["n_train"])
+    a = _single(frames, n_train, cfg)
+    b = train_band_engine(frames[:n_train], cfg, (0, frames.shape[2]))
+    for nm in STATE:
+        assert np.array_equal(getattr(a, nm), getattr(b, nm)), nm
+    assert np.array_equal(a.tables, b.tables)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_batch_engine_equals_separate_engines(dtype):
+    from paper_1705_09339_b200 import synth
+    from paper_1705_09339_b200.parallel import BatchEngine
+    spec = synth.small_spec(5, 40, 24, 60, 30)
+    scenes = [synth.Scene(spec.for_stream(i)) for i in range(3)]
+    seqs = [sc.frames(0, 60) for sc in scenes]
+    cfg = config_for({"k_max": 5, "color": True, "reorder_interval": 12,
+                      "clusters": 3}, state_dtype=dtype)
+    singles = [_single(s, 30, cfg) for s in seqs]
+    batch = BatchEngine.train([s[:30] for s in seqs], cfg)
+    for t in range(30, 60):
+        masks, stats = batch.process_frames(np.stack([s[t] for s in seqs]))
+        for i, eng in enumerate(singles):
+            m, st = eng.process_frame(seqs[i][t])
+            assert np.array_equal(masks[i], m.labels), (i, t)
+            assert stats[i].tolist() == st.as_row(), (i, t)
+    for i, eng in enumerate(singles):
+        got = batch.export_stream(i)
+        for nm in STATE:
+            assert np.array_equal(got[nm], getattr(eng, nm)), (i, nm)

@@ -20,7 +20,9 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SO_PATH = PKG / "libcog_b200.so"
 SOURCES = [PKG / "csrc" / "cog_kernels.cu"]
-HEADERS = [PKG / "csrc" / "cog_device.cuh", ROOT / "include" / "cog_b200.h"]
+# every header the translation unit includes (a stale .so after editing one
+# of them would silently run old code)
+HEADERS = sorted((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "cog_b200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -70,6 +70,7 @@ struct StepArgs {
   int reorder_now;
   int fuse_finalize;
   int cw, iters, tiles_x, n_tiles;
+  int union_mask;  // deep kernel forms the mask from every plane's label bit
 };
 
 template <typename T>
@@ -415,6 +416,7 @@ __device__ __forceinline__ void preload_r2(const PlaneRef<T>& pr, size_t p,
 // reference's, while continuous values (conf, rho) carry fp32 rounding.
 // ---------------------------------------------------------------------------
 constexpr float FILTER_MARGIN = 1e-5f;
+constexpr float MATCH_ABS_MARGIN = 3e-5f;  // > fp32 rounding of |v - mu| (v <= 255)
 
 // reference form: |v - mu| <= lam * sqrt(var)
 __device__ __noinline__ bool match_exact(double v, double mu, double var,
@@ -581,9 +583,9 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
     const float g1 = fabsf(vf - (float)pre.mu1) - thr1;
     t0 = g0 <= 0.0f;
     t1 = g1 <= 0.0f;
-    if (fabsf(g0) <= FILTER_MARGIN * thr0)
+    if (fabsf(g0) <= FILTER_MARGIN * thr0 + MATCH_ABS_MARGIN)
       t0 = match_exact(v, (double)pre.mu0, (double)pre.var0, q.match_lambda);
-    if (fabsf(g1) <= FILTER_MARGIN * thr1)
+    if (fabsf(g1) <= FILTER_MARGIN * thr1 + MATCH_ABS_MARGIN)
       t1 = match_exact(v, (double)pre.mu1, (double)pre.var1, q.match_lambda);
   } else {
     // binary64 throughout, the reference's operation order
@@ -1608,12 +1610,50 @@ __global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
       pr.meta[p] = (uint16_t)nm;
       if (lbl) {
         pr.dyn[p] |= 1u << 8;
-        const uintptr_t addr = (uintptr_t)(mask + p);
-        unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
-        const unsigned sh = (unsigned)(addr & 3) * 8;
-        const unsigned old = atomicOr(word, 0xFFu << sh);
-        fg += ((old >> sh) & 0xFFu) == 0u;
+        if (!a.union_mask) {
+          const uintptr_t addr = (uintptr_t)(mask + p);
+          unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
+          const unsigned sh = (unsigned)(addr & 3) * 8;
+          const unsigned old = atomicOr(word, 0xFFu << sh);
+          fg += ((old >> sh) & 0xFFu) == 0u;
+        }
       }
+    }
+  }
+  if (a.union_mask) {
+    // every plane-pixel's label is final once all CTAs of this stream have
+    // run their items: stream-wide barrier (the grid is co-resident), then
+    // mask = OR over planes of the label bit (dyn bit 8), 4 pixels a thread
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(sync + 2, 1u);
+      while (*(volatile uint32_t*)(sync + 2) < gridDim.x) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+    const uint32_t* dyn = a.s.dyn + (size_t)s * d * P;
+    const size_t nq = (P % 4 == 0) ? P / 4 : 0;  // 16-B aligned planes
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
+         i += (size_t)gridDim.x * blockDim.x) {
+      unsigned lab = 0;
+      for (int c = 0; c < d; ++c) {
+        const uint4 v = __ldcg((const uint4*)(dyn + (size_t)c * P) + i);
+        lab |= ((v.x >> 8) & 1u) | ((v.y >> 7) & 2u) | ((v.z >> 6) & 4u) |
+               ((v.w >> 5) & 8u);
+      }
+      ((unsigned*)mask)[i] = (lab & 1u ? 0xFFu : 0u) |
+                             (lab & 2u ? 0xFF00u : 0u) |
+                             (lab & 4u ? 0xFF0000u : 0u) |
+                             (lab & 8u ? 0xFF000000u : 0u);
+      fg += __popc(lab);
+    }
+    for (size_t q = nq * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+         q < P; q += (size_t)gridDim.x * blockDim.x) {
+      unsigned lab = 0;
+      for (int c = 0; c < d; ++c) lab |= (dyn[(size_t)c * P + q] >> 8) & 1u;
+      mask[q] = lab ? 255 : 0;
+      fg += lab;
     }
   }
   for (int o = 16; o > 0; o >>= 1) fg += __shfl_xor_sync(FULL, fg, o);
@@ -2011,6 +2051,8 @@ __global__ void import_kernel(cog_geom g, cog_state s, cog_ref_state in) {
 }
 
 #include "cog_lean.cuh"
+#include "cog_fast.cuh"
+#include "cog_vec.cuh"
 
 // ---------------------------------------------------------------------------
 // host helpers
@@ -2115,7 +2157,8 @@ int kernel_choice() {
   if (!e) return 0;
   if (e[0] == 'p') return 1;
   if (e[0] == 'g') return 2;
-  return 0;
+  if (e[0] == 'l') return 3;
+  return 0;  // "fast" / "vec" and default
 }
 
 template <typename T>
@@ -2131,7 +2174,8 @@ StepFn<T> pick_lean(int K, int d) {
 }
 
 bool lean_ok(const StepArgs& a) {
-  return kernel_choice() == 0 && a.iters == 1 &&
+  const int kc = kernel_choice();
+  return (kc == 0 || kc == 3) && a.iters == 1 &&
          (a.g.depth == 1 || a.g.depth == 3) && a.g.stride <= 5;
 }
 
@@ -2162,6 +2206,74 @@ bool pipe_ok(const StepArgs& a) {
          (a.g.width % 4) == 0 && ((uintptr_t)a.frame % 4) == 0;
 }
 
+template <int KMAX>
+int launch_fast_k(const StepArgs& a, cudaStream_t st) {
+  auto fn = fast_kernel<KMAX>;
+  const size_t smem = fast_smem_bytes(a.g.depth, a.g.n_groups);
+  if (smem > 200 * 1024) return COG_EUNSUPPORTED;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, LEAN_THREADS, smem);
+  if (occ < 1) occ = 1;
+  // balanced static schedule: t units per warp, just enough CTAs
+  const long long units = (long long)a.n_tiles * a.g.depth;
+  const int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
+  const long long slots = (long long)per_stream * LEAN_WARPS;
+  const long long t = (units + slots - 1) / slots;
+  int gx = (int)((units + t * LEAN_WARPS - 1) / (t * LEAN_WARPS));
+  if (gx < 1) gx = 1;
+  const FastConst k = make_fast_const(a.q);
+  fn<<<dim3(gx, a.g.streams), LEAN_THREADS, smem, st>>>(a, k);
+  return launch_status();
+}
+
+template <int KMAX>
+int launch_vec_k(const StepArgs& a, cudaStream_t st) {
+  auto fn = vec_kernel<KMAX>;
+  const size_t smem = fast_smem_bytes(a.g.depth, a.g.n_groups);
+  if (smem > 200 * 1024) return COG_EUNSUPPORTED;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, LEAN_THREADS, smem);
+  if (occ < 1) occ = 1;
+  const int tile_w = 4 * (32 / a.g.stride);
+  const long long tiles = (long long)((a.g.width + tile_w - 1) / tile_w) *
+                          ((a.g.height + a.g.stride - 1) / a.g.stride);
+  const long long units = tiles * a.g.depth;
+  const int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
+  const long long slots = (long long)per_stream * LEAN_WARPS;
+  const long long t = (units + slots - 1) / slots;
+  int gx = (int)((units + t * LEAN_WARPS - 1) / (t * LEAN_WARPS));
+  if (gx < 1) gx = 1;
+  const FastConst k = make_fast_const(a.q);
+  fn<<<dim3(gx, a.g.streams), LEAN_THREADS, smem, st>>>(a, k);
+  return launch_status();
+}
+
+bool vec_ok(const StepArgs& a) {
+  // experimental (COG_KERNEL=vec): 4 pixels a lane with 16-B accesses
+  const char* e = getenv("COG_KERNEL");
+  if (!e || e[0] != 'v') return false;
+  const int st = a.g.stride;
+  return (st == 1 || st == 2 || st == 4) && a.g.width % 4 == 0 &&
+         ((uintptr_t)a.frame % 16) == 0;
+}
+
+int launch_fast(const StepArgs& a, cudaStream_t st) {
+  if (vec_ok(a)) {
+    if (a.g.k <= 3) return launch_vec_k<3>(a, st);
+    if (a.g.k <= 5) return launch_vec_k<5>(a, st);
+    return launch_vec_k<8>(a, st);
+  }
+  if (a.g.k <= 3) return launch_fast_k<3>(a, st);
+  if (a.g.k <= 5) return launch_fast_k<5>(a, st);
+  return launch_fast_k<8>(a, st);
+}
+
 template <typename T>
 int launch_hot(const StepArgs& a, cudaStream_t st) {
   if (lean_ok(a)) return launch_lean<T>(a, st);
@@ -2189,19 +2301,53 @@ int launch_hot(const StepArgs& a, cudaStream_t st) {
   return launch_status();
 }
 
+bool fast_ok(const StepArgs& a, bool f32) {
+  const unsigned long long span = (unsigned long long)a.g.streams *
+                                  a.g.depth * (a.g.k > 5 ? a.g.k : 5) *
+                                  (unsigned long long)a.g.height * a.g.width;
+  return f32 && kernel_choice() == 0 && a.iters == 1 && a.g.stride <= 5 &&
+         span < (1ull << 32) && !a.q.exact_group_sums;
+}
+
+template <typename T>
+int launch_deep(StepArgs a, cudaStream_t st, bool union_mask) {
+  auto fn = pick_deep<T>(a.g.k);
+  a.union_mask = union_mask ? 1 : 0;
+  const size_t P = (size_t)a.g.height * a.g.width;
+  size_t dg = (P * a.g.depth / 8 + 255) / 256;  // covers ~12% deep items
+  if (!union_mask) {
+    const size_t cap = (size_t)num_sms() * 8 / a.g.streams + 1;
+    if (dg > cap) dg = cap;
+    if (dg < 1) dg = 1;
+    fn<<<dim3((unsigned)dg, a.g.streams), 256, 0, st>>>(a);
+    return launch_status();
+  }
+  // the union pass needs a stream-wide barrier: cooperative launch of a
+  // grid that is guaranteed co-resident
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0);
+  if (occ < 1) occ = 1;
+  const size_t cap = (size_t)num_sms() * occ / a.g.streams;
+  if (cap < 1) return COG_EUNSUPPORTED;
+  const size_t want = (P / 4 + 255) / 256;  // union pass: 4 pixels a thread
+  if (dg < want) dg = want;
+  if (dg > cap) dg = cap;
+  if (dg < 1) dg = 1;
+  void* args[] = {(void*)&a};
+  cudaError_t e = cudaLaunchCooperativeKernel(
+      (const void*)fn, dim3((unsigned)dg, a.g.streams), dim3(256), args, 0, st);
+  return e == cudaSuccess ? COG_OK : (int)e;
+}
+
 template <typename T>
 int launch_step(const StepArgs& a, cudaStream_t st) {
   set_fetch_granularity();
-  int rc = launch_hot<T>(a, st);
+  // float32 state: the plane kernel, mask formed by the deep kernel's union
+  // pass; otherwise lean / pipelined / general with the mask written inline
+  const bool fast = fast_ok(a, sizeof(T) == 4);
+  int rc = fast ? launch_fast(a, st) : launch_hot<T>(a, st);
   if (rc) return rc;
-  // deep pass: fixed persistent grid (the worklist length is on the device)
-  const size_t P = (size_t)a.g.height * a.g.width;
-  size_t dg = (P * a.g.depth / 8 + 255) / 256;  // covers ~12% deep items
-  const size_t cap = (size_t)num_sms() * 8 / a.g.streams + 1;
-  if (dg > cap) dg = cap;
-  if (dg < 1) dg = 1;
-  pick_deep<T>(a.g.k)<<<dim3((unsigned)dg, a.g.streams), 256, 0, st>>>(a);
-  return launch_status();
+  return launch_deep<T>(a, st, fast);
 }
 
 }  // namespace

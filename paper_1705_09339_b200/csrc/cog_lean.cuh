@@ -189,7 +189,11 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_LEAN_MINB)
                                     eps);
       if (ev) {
         const uint32_t o = (uint32_t)c * P + p;
+#ifdef COG_EXP_NOTABLE
+        pre[c].tv = 0.01f * (float)(o & 7);  // ablation: no table gather
+#else
         pre[c].tv = __ldcg(tabb + (size_t)o * 256 + pre[c].vb);
+#endif
         const int r0 = meta_ref(pre[c].meta, 0), r1 = meta_ref(pre[c].meta, 1);
         const size_t mb = (size_t)c * K * P + p;
         pre[c].mu0 = mub[mb + (size_t)r0 * P];

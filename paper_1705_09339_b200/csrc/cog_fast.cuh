@@ -1,12 +1,15 @@
 // cog_fast.cuh -- the float32-state step kernel (the throughput path).
 // Included inside the anonymous namespace of cog_kernels.cu.
 //
-// Work unit = one plane of one stride-aligned warp tile; thread = one
-// plane-pixel.  Planes are independent in the reference (cascade.py:281),
-// so a warp never holds more than one plane's state: ~40-50 registers, high
-// occupancy, one dependent load round per unit.  The only cross-plane
-// result, the union foreground mask, is formed by the deep kernel's union
-// pass from every plane's final label bit (dyn bit 8), after the worklist.
+// Work unit = one stride-aligned warp tile (stride rows x cw columns, so
+// every copy pixel's anchor is in row 0 of the same warp); thread = one
+// pixel, planes processed one after another in a non-unrolled loop (the
+// reference's planes are independent, cascade.py:281) so a thread holds one
+// plane's state at a time.  The union mask is written per tile; labels that
+// arrive with the deep kernel (GMM fall-throughs) are OR-ed in there.
+// (Measured alternatives: one plane per warp with the
+// mask formed in a union pass, and 4 pixels per lane with 16-B accesses --
+// both slower on B200.)
 // The per-plane-pixel work is split by frequency:
 //   * fast path (the common case: evaluated pixel, sampling clock idle, not
 //     compat, no decision within the filter margin): the cascade written
@@ -49,10 +52,10 @@ FastConst make_fast_const(const cog_params& q) {
 
 // out-of-line general path for the rare plane-pixels (returns by value:
 // taking the address of the caller's HotOut would pin it to local memory)
-#ifdef COG_SLOW_INLINE
-#define COG_SLOW_ATTR __forceinline__
-#else
+#ifdef COG_SLOW_CALL
 #define COG_SLOW_ATTR __noinline__
+#else
+#define COG_SLOW_ATTR __forceinline__  // measured faster than a call
 #endif
 template <typename T>
 __device__ COG_SLOW_ATTR HotOut hot_px_slow(const StepArgs* __restrict__ a,
@@ -94,17 +97,17 @@ __device__ __forceinline__ int fmatch(float vf, float mu, float thr) {
 }
 
 #ifndef COG_FAST_MINB
-#define COG_FAST_MINB 4
+#define COG_FAST_MINB 3
 #endif
 
-template <int KMAX>
+template <int KMAX, int D>
 __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
     fast_kernel(const __grid_constant__ StepArgs a,
                 const __grid_constant__ FastConst k) {
   using T = float;
   extern __shared__ double s_mem[];
   const int s = blockIdx.y;
-  const int D = a.g.depth, G = a.g.n_groups, K = a.g.k;
+  const int G = a.g.n_groups, K = a.g.k;
   const int H = a.g.height, W = a.g.width, stride = a.g.stride;
   const uint32_t P = (uint32_t)H * (uint32_t)W;
   const int words = acc_words(D, G);
@@ -177,52 +180,79 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
   int kc_units = 0;
   int wq_n = 0;
 
-  // static, balanced assignment of (tile, plane) units; consecutive warps
-  // take the planes of one tile, then the next tile
-  const int n_units = a.n_tiles * D;
+  // static, balanced tile assignment (the launcher sizes the grid so every
+  // warp gets the same number of tiles); tile j of warp gw is gw + j * nw
   const int nw = gridDim.x * LEAN_WARPS;
-  for (int u = blockIdx.x * LEAN_WARPS + warp; u < n_units; u += nw) {
-    const int wt = u / D, c = u - wt * D;
-    const int ty = wt / a.tiles_x, tx = wt - ty * a.tiles_x;
+  int wt = blockIdx.x * LEAN_WARPS + warp;
+  int ty = wt / a.tiles_x, tx = wt - ty * a.tiles_x;
+  const int dty = nw / a.tiles_x, dtx = nw - dty * a.tiles_x;
+  const int kc_flush = 511 / D;  // D counts per tile per 9-bit field
+  unsigned fg_count = 0;
+  for (; wt < a.n_tiles; wt += nw) {
     const int y = ty * stride + lrow, x_ = tx * cw + lcol;
+    tx += dtx;
+    ty += dty;
+    if (tx >= a.tiles_x) {
+      tx -= a.tiles_x;
+      ty += 1;
+    }
     const bool valid = lane_ok && y < H && x_ < W;
     const uint32_t p = valid ? (uint32_t)y * (uint32_t)W + (uint32_t)x_ : 0u;
-    const uint32_t o = sP + (uint32_t)c * P + p;
-    const uint32_t mb = (sK + c) * K * P + p;  // mode 0 of this plane-pixel
 
     if (do_reset || do_reorder) {
       if (valid) {
-        const PlaneRef<T> pr = plane_ref<T>(a, s, c);
         const int g0 = a.s.gid[s1 + p];
         const bool mem = G > 0 && g0 != (int)UNGROUPED;
-        if (do_reset) cold_reset<T, KMAX>(pr, p, a.q.initial_variance);
-        if (do_reorder)
-          cold_reorder<T>(pr, p, mem ? s_gmu[c * G + g0]
-                                     : (G > 0 ? s_gmu[c * G] : 0.0));
+#pragma unroll 1
+        for (int c = 0; c < D; ++c) {
+          const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+          if (do_reset) cold_reset<T, KMAX>(pr, p, a.q.initial_variance);
+          if (do_reorder)
+            cold_reorder<T>(pr, p, mem ? s_gmu[c * G + g0]
+                                       : (G > 0 ? s_gmu[c * G] : 0.0));
+        }
       }
       __syncwarp();
     }
-
-    // ---- round 1: pixel-indexed loads
     const int gid = valid ? (int)a.s.gid[s1 + p] : (int)UNGROUPED;
     const int cls = valid ? (int)a.s.cls[s1 + p] : 0;
-    Pre<T> x;
-    x.vb = 0;
-    x.dyn = x.meta = x.streak = 0u;
-    x.peak = 1.0f;
-    x.tv = 0.0f;
-    x.mu0 = x.mu1 = 0.0f;
-    x.var0 = x.var1 = 1.0f;
-    if (valid) {
-      x.vb = a.frame[o];
-      x.dyn = a.s.dyn[o];
-      x.meta = a.s.meta[o];
-      x.streak = a.s.streak[o];
-      x.peak = __ldg(a.s.peak + o);
-    }
     const bool member = valid && G > 0 && gid != (int)UNGROUPED;
     const float wa = k.w[3 * cls], wb = k.w[3 * cls + 1], wc = k.w[3 * cls + 2];
     const unsigned any_member = __ballot_sync(FULL, member);
+    int fg = 0;
+
+    // round 1 of every plane up front (pixel-indexed loads), then the
+    // planes one at a time in a non-unrolled loop (the reference's planes
+    // are independent, cascade.py:281): one dependent load round per plane,
+    // a small register footprint
+    Pre<T> n0, n1, n2;
+    auto load1 = [&](int c, Pre<T>& x) {
+      x.vb = 0;
+      x.dyn = x.meta = x.streak = 0u;
+      x.peak = 1.0f;
+      if (valid) {
+        const uint32_t o = sP + (uint32_t)c * P + p;
+        x.vb = a.frame[o];
+        x.dyn = a.s.dyn[o];
+        x.meta = a.s.meta[o];
+        x.streak = a.s.streak[o];
+        x.peak = __ldg(a.s.peak + o);
+      }
+    };
+    load1(0, n0);
+    if (D > 1) load1(1, n1);
+    if (D > 2) load1(2, n2);
+#pragma unroll 1
+    for (int c = 0; c < D; ++c) {
+    const uint32_t o = sP + (uint32_t)c * P + p;
+    const uint32_t mb = (sK + c) * K * P + p;  // mode 0 of this plane-pixel
+    Pre<T> x = n0;
+    if (D > 1) n0 = n1;
+    if (D > 2) n1 = n2;
+    x.tv = 0.0f;
+    x.mu0 = x.mu1 = 0.0f;
+    x.var0 = x.var1 = 1.0f;
+
     // ---- round 2: table entry at v, the MEAN / MEANVAR modes
     if (valid && !compat &&
         will_evaluate(sampling, x.dyn, x.vb, on_lat, a.q.chp_epsilon)) {
@@ -438,6 +468,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
       label = al;
       a.s.dyn[o] = ho.dyn | ((uint32_t)al << 8);
     }
+    fg |= label;
 
     // ---- group partials (exact sums) into the warp's private slice
 #ifdef COG_EXP_NOGROUP
@@ -480,7 +511,11 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
       }
     }
   
-    if (++kc_units >= 511) {
+    }  // planes
+
+    if (valid) a.mask[s1 + p] = fg ? 255 : 0;
+    fg_count += __popc(__ballot_sync(FULL, valid && fg));
+    if (++kc_units >= kc_flush) {
 #pragma unroll
       for (int q = 0; q < 7; ++q) {
         const unsigned v = warp_sum_u32((unsigned)((kc >> (9 * q)) & 511u));
@@ -505,6 +540,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
     const unsigned v = warp_sum_u32((unsigned)((kc >> (9 * q)) & 511u));
     if (lane == 0) wacc[acc_kind(0, q)] += v;
   }
+  if (lane == 0) wacc[acc_fg(D)] += fg_count;
   __syncthreads();
   unsigned long long* gacc = (unsigned long long*)a.s.accum + (size_t)s * words;
   for (int i = threadIdx.x; i < words; i += LEAN_THREADS) {

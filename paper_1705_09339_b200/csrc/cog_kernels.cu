@@ -2206,9 +2206,9 @@ bool pipe_ok(const StepArgs& a) {
          (a.g.width % 4) == 0 && ((uintptr_t)a.frame % 4) == 0;
 }
 
-template <int KMAX>
+template <int KMAX, int D>
 int launch_fast_k(const StepArgs& a, cudaStream_t st) {
-  auto fn = fast_kernel<KMAX>;
+  auto fn = fast_kernel<KMAX, D>;
   const size_t smem = fast_smem_bytes(a.g.depth, a.g.n_groups);
   if (smem > 200 * 1024) return COG_EUNSUPPORTED;
   if (smem > 48 * 1024)
@@ -2217,8 +2217,8 @@ int launch_fast_k(const StepArgs& a, cudaStream_t st) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, LEAN_THREADS, smem);
   if (occ < 1) occ = 1;
-  // balanced static schedule: t units per warp, just enough CTAs
-  const long long units = (long long)a.n_tiles * a.g.depth;
+  // balanced static schedule: t tiles per warp, just enough CTAs
+  const long long units = (long long)a.n_tiles;
   const int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
   const long long slots = (long long)per_stream * LEAN_WARPS;
   const long long t = (units + slots - 1) / slots;
@@ -2269,9 +2269,14 @@ int launch_fast(const StepArgs& a, cudaStream_t st) {
     if (a.g.k <= 5) return launch_vec_k<5>(a, st);
     return launch_vec_k<8>(a, st);
   }
-  if (a.g.k <= 3) return launch_fast_k<3>(a, st);
-  if (a.g.k <= 5) return launch_fast_k<5>(a, st);
-  return launch_fast_k<8>(a, st);
+  if (a.g.depth == 1) {
+    if (a.g.k <= 3) return launch_fast_k<3, 1>(a, st);
+    if (a.g.k <= 5) return launch_fast_k<5, 1>(a, st);
+    return launch_fast_k<8, 1>(a, st);
+  }
+  if (a.g.k <= 3) return launch_fast_k<3, 3>(a, st);
+  if (a.g.k <= 5) return launch_fast_k<5, 3>(a, st);
+  return launch_fast_k<8, 3>(a, st);
 }
 
 template <typename T>
@@ -2306,7 +2311,8 @@ bool fast_ok(const StepArgs& a, bool f32) {
                                   a.g.depth * (a.g.k > 5 ? a.g.k : 5) *
                                   (unsigned long long)a.g.height * a.g.width;
   return f32 && kernel_choice() == 0 && a.iters == 1 && a.g.stride <= 5 &&
-         span < (1ull << 32) && !a.q.exact_group_sums;
+         (a.g.depth == 1 || a.g.depth == 3) && span < (1ull << 32) &&
+         !a.q.exact_group_sums;
 }
 
 template <typename T>
@@ -2342,12 +2348,12 @@ int launch_deep(StepArgs a, cudaStream_t st, bool union_mask) {
 template <typename T>
 int launch_step(const StepArgs& a, cudaStream_t st) {
   set_fetch_granularity();
-  // float32 state: the plane kernel, mask formed by the deep kernel's union
-  // pass; otherwise lean / pipelined / general with the mask written inline
+  // float32 state: the fast kernel (vec: 4 pixels a lane, mask formed by
+  // the deep kernel's union pass); otherwise lean / pipelined / general
   const bool fast = fast_ok(a, sizeof(T) == 4);
   int rc = fast ? launch_fast(a, st) : launch_hot<T>(a, st);
   if (rc) return rc;
-  return launch_deep<T>(a, st, fast);
+  return launch_deep<T>(a, st, fast && vec_ok(a));
 }
 
 }  // namespace

@@ -1,11 +1,14 @@
 """Benchmark of the CoG hot path (BASELINE.json metric: pixel-frames/s of
 classify+update, and % of HBM roofline).
 
-Workload (N=1): BASELINE config C2 -- 640x480 RGB, K=3, trained on the
-first 200 frames of the seeded synthetic scene (paper_1705_09339_b200.synth);
-a step is one frame through the fused step kernel.  For N>1 every rank runs
-its own independent C2-shaped stream (seed 1+rank, no collectives: weak
-scaling), timed on the device and reduced with MAX over ranks.
+Workload (N=1, default): BASELINE config C2 -- 640x480 RGB, K=3, trained
+on the first 200 frames of the seeded synthetic scene
+(paper_1705_09339_b200.synth); a step is one frame through the step kernels.
+For N>1 every rank runs its own independent C2-shaped stream (seed 1+rank,
+no collectives: weak scaling), timed on the device, MAX over ranks.
+--workload c3 / c4 / c5 measure the other BASELINE configs (c4 at N>1: one
+4K stream in row bands with a per-frame NCCL all-reduce, strong scaling;
+c5: a batch engine of independent 720p streams).
 
 value    device-resident frames, CUDA events around each step's launch on the
          engine stream, L2 flushed (256 MiB write) between steps (outside
@@ -172,8 +175,10 @@ def cpu_baseline(frames, eng, cfg, n_frames, threads):
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port) on the
-    same workload, all host threads, rank 0 only."""
+    """--impl reference: the reference's CPU path (the oracle port of its
+    numba kernels, all host threads) on the same workload; rank 0 only.
+    c4 runs a 270-row band (1/8) of the 4K frame: the full frame needs
+    ~100 GB of host RAM in the reference's layout."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -181,19 +186,26 @@ def run_reference(args):
     from oracle import oracle as orc
     from paper_1705_09339_b200 import synth
     from paper_1705_09339_b200.config import EngineConfig
-    spec = synth.CONFIGS[2]
+    cid = {"c2": 2, "c3": 3, "c4": 4, "c5": 5}[args.workload]
+    spec = synth.CONFIGS[cid].for_stream(0)
     cores = len(os.sched_getaffinity(0))
     os.environ["COG_ORACLE_THREADS"] = str(cores)
     scene = synth.Scene(spec)
     n_train = spec.training
-    train = scene.frames(0, n_train)
+    workers = max(1, min(16, cores))
+    train = scene.frames(0, n_train, workers)
+    run = scene.frames(n_train, n_train + args.warmup + args.steps, workers)
+    band = ""
+    if cid == 4:
+        train = np.ascontiguousarray(train[:, :, :270])
+        run = np.ascontiguousarray(run[:, :, :270])
+        band = " (rows 0-269 of the 4K frame)"
     cfg = EngineConfig(k_max=spec.k_max, color=True,
                        training_frames=n_train).validate()
     t0 = time.perf_counter()
     eng = orc.train(train, cfg)
     t_train = time.perf_counter() - t0
     eng.threads = cores
-    run = scene.frames(n_train, n_train + args.warmup + args.steps)
     for f in run[:args.warmup]:
         eng.process(f)
     times = []
@@ -209,19 +221,160 @@ def run_reference(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded C2 generator)",
-        "config": {"workload": "C2 640x480x3 K=3 N=200 (BASELINE configs[1])",
-                   "frames": "post-training frames 200.."},
+        "data": "synthetic (seeded BASELINE generator)",
+        "config": {"workload": f"{args.workload.upper()} "
+                               f"{spec.width}x{spec.height}x3 K={spec.k_max} "
+                               f"N={n_train}{band}",
+                   "frames": f"post-training frames {n_train}.."},
         "cpu_baseline": {"value": value, "unit": "pixel-frames/s",
                          "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} C2 frames after "
-                                   f"{args.warmup} warm-up frames; oracle "
-                                   f"training {t_train:.1f}s excluded"},
+                         "sample": f"{args.steps} frames after {args.warmup} "
+                                   f"warm-up frames{band}; oracle C kernels "
+                                   f"(restatement of the reference's numba "
+                                   f"kernels, pixels split over {cores} "
+                                   f"threads); training {t_train:.1f}s "
+                                   f"excluded"},
         "e2e": {"value": value, "unit": "pixel-frames/s",
                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
     return 0
+
+
+class Workload:
+    """One bench workload: a trained engine plus its frame sources.
+
+    c2 (default, BASELINE configs[1]): one 640x480x3 stream per rank.
+    c3: one 1920x1080x3 stream per rank (K=5).
+    c4: one 3840x2160x3 stream; at N>1 split into stride-aligned row bands,
+        one per rank, partials all-reduced over NCCL each frame.
+    c5: independent 1280x720x3 streams (K=5), `streams` resident per rank
+        in one batch engine (64 / N in total, waves of <= 32 on one GPU).
+    """
+
+    def __init__(self, name, args, world, rank):
+        import torch
+        from paper_1705_09339_b200 import synth
+        from paper_1705_09339_b200.config import EngineConfig
+        from paper_1705_09339_b200.training import train_engine
+        self.name = name
+        cid = {"c2": 2, "c3": 3, "c4": 4, "c5": 5}[name]
+        base = synth.CONFIGS[cid]
+        workers = max(1, min(16, len(os.sched_getaffinity(0))))
+        total_steps = args.warmup + args.steps
+        self.extra_frames = 2 * total_steps
+        t0 = time.perf_counter()
+        if name in ("c2", "c3"):
+            spec = base.for_stream(rank)
+            sc = synth.Scene(spec)
+            train = sc.frames(0, spec.training, workers)
+            self.cfg = EngineConfig(k_max=spec.k_max, color=True,
+                                    training_frames=spec.training,
+                                    state_dtype=args.state).validate()
+            self.t_gen = time.perf_counter() - t0
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            self.eng = train_engine(train, self.cfg)
+            torch.cuda.synchronize()
+            self.t_train = time.perf_counter() - t0
+            self.host = sc.frames(spec.training,
+                                  spec.training + self.extra_frames, workers)
+            self.streams, self.spec = 1, spec
+            self.pixels = spec.n_pix            # per rank per step
+            self.workload = (f"{name.upper()} {spec.width}x{spec.height}x3 "
+                             f"K={spec.k_max} N={spec.training}")
+        elif name == "c4":
+            from paper_1705_09339_b200.parallel import (
+                DistReducer, band_rows, dist_gather_rows, train_band_engine)
+            spec = base
+            sc = synth.Scene(spec)
+            train = sc.frames(0, spec.training, workers)
+            self.cfg = EngineConfig(k_max=spec.k_max, color=True,
+                                    training_frames=spec.training,
+                                    state_dtype=args.state).validate()
+            self.t_gen = time.perf_counter() - t0
+            rows = band_rows(spec.height, world, self.cfg.stride)[rank]
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            self.eng = train_band_engine(
+                train, self.cfg, rows,
+                gather=dist_gather_rows() if world > 1 else None)
+            if world > 1:
+                self.eng.reducer = DistReducer()
+            torch.cuda.synchronize()
+            self.t_train = time.perf_counter() - t0
+            full = sc.frames(spec.training, spec.training + self.extra_frames,
+                             workers)
+            self.host = np.ascontiguousarray(full[:, :, rows[0]:rows[1]])
+            self.streams, self.spec = 1, spec
+            self.pixels = (rows[1] - rows[0]) * spec.width
+            self.workload = (f"C4 3840x2160x3 K=5 N=150, rows {rows[0]}-"
+                             f"{rows[1]} of 2160 on this rank")
+        else:
+            from paper_1705_09339_b200.parallel import BatchEngine, streams_for_rank
+            mine = streams_for_rank(64, rank, world)[:args.streams]
+            specs = [base.for_stream(i) for i in mine]
+            scenes = [synth.Scene(sp) for sp in specs]
+            trains = [sc.frames(0, base.training, workers) for sc in scenes]
+            self.cfg = EngineConfig(k_max=base.k_max, color=True,
+                                    training_frames=base.training,
+                                    state_dtype=args.state).validate()
+            self.t_gen = time.perf_counter() - t0
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            self.eng = BatchEngine.train(trains, self.cfg)
+            torch.cuda.synchronize()
+            self.t_train = time.perf_counter() - t0
+            del trains
+            per = [sc.frames(base.training, base.training + self.extra_frames,
+                             workers) for sc in scenes]
+            self.host = np.ascontiguousarray(np.stack(per, axis=1))  # (T,S,d,H,W)
+            self.streams, self.spec = len(mine), base
+            self.pixels = len(mine) * base.n_pix
+            self.workload = (f"C5 {len(mine)} x 1280x720x3 K=5 N=100 streams "
+                             f"resident on this rank (seeds {specs[0].seed}-"
+                             f"{specs[-1].seed})")
+        self.dev_frames = [torch.from_numpy(f).cuda() for f in self.host]
+        dev = torch.device("cuda", torch.cuda.current_device())
+        if self.streams == 1:
+            h, w = self.dev_frames[0].shape[1:]
+            self.mask = torch.empty((h, w), dtype=torch.uint8, device=dev)
+            self.stats = torch.empty((total_steps, 16), dtype=torch.int64,
+                                     device=dev)
+        else:
+            h, w = self.dev_frames[0].shape[2:]
+            self.mask = torch.empty((self.streams, h, w), dtype=torch.uint8,
+                                    device=dev)
+            self.stats = torch.empty((total_steps, self.streams, 16),
+                                     dtype=torch.int64, device=dev)
+
+    def step(self, i, j):
+        """Frame i of the device-resident set, stats slot j."""
+        f = self.dev_frames[i % len(self.dev_frames)]
+        if self.streams == 1:
+            self.eng.process_frame_device(f, self.mask, self.stats[j])
+        else:
+            self.eng.process_frames_device(f, self.mask, self.stats[j])
+
+    def rows(self, lo):
+        r = self.stats[lo:].cpu().numpy()
+        return r.reshape(-1, 16)
+
+    def e2e_engine(self):
+        return self.eng.clone() if hasattr(self.eng, "clone") else self.eng
+
+    def e2e_step(self, eng, i):
+        """Public API from host memory, result read back: returns bytes in,
+        bytes out."""
+        from paper_1705_09339_b200.frame_io import Frame
+        f = self.host[i % len(self.host)]
+        if self.streams == 1:
+            m, st = eng.process_frame(Frame.from_array(f, i))
+            m.labels
+            st.n_foreground
+            return f.nbytes, m.labels.nbytes + 16 * 8
+        masks, stats = eng.process_frames(f)
+        return f.nbytes, masks.nbytes + stats.nbytes
 
 
 def main():
@@ -230,6 +383,9 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="cog", choices=["cog", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--streams", type=int, default=32,
+                    help="c5: resident streams per rank (<= 64 / N)")
     ap.add_argument("--state", default="float32",
                     choices=["float32", "float64"])
     ap.add_argument("--cpu-frames", type=int, default=20)
@@ -242,39 +398,21 @@ def main():
         return run_reference(args)
 
     import torch
-    from paper_1705_09339_b200 import synth
-    from paper_1705_09339_b200.config import EngineConfig
-    from paper_1705_09339_b200.frame_io import Frame
-    from paper_1705_09339_b200.training import train_engine
 
     world, rank, local = dist_setup()
-    spec = synth.CONFIGS[2].for_stream(rank)
-    scene = synth.Scene(spec)
-    n_train = spec.training
-    cfg = EngineConfig(k_max=spec.k_max, color=True, training_frames=n_train,
-                       state_dtype=args.state).validate()
-    t0 = time.perf_counter()
-    train = scene.frames(0, n_train)
-    t_gen = time.perf_counter() - t0
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    eng = train_engine(train, cfg)
-    torch.cuda.synchronize()
-    t_train = time.perf_counter() - t0
+    wl = Workload(args.workload, args, world, rank)
+    eng, cfg = wl.eng, wl.cfg
     total_steps = args.warmup + args.steps
-    host_frames = scene.frames(n_train, n_train + 2 * total_steps)
-    dev_frames = [torch.from_numpy(f).cuda() for f in host_frames]
-    e2e_eng = eng.clone()
     dev = torch.device("cuda", torch.cuda.current_device())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    mask = torch.empty((spec.height, spec.width), dtype=torch.uint8, device=dev)
-    stats = torch.empty((total_steps, 16), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
+    e2e_eng = wl.e2e_engine()
+    launches_per_step = 2  # hot kernel + deep/finalize kernel
 
     # ---- device-resident loop
     for i in range(args.warmup):
         flush.zero_()
-        eng.process_frame_device(dev_frames[i], mask, stats[i])
+        wl.step(i, i)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
@@ -284,8 +422,7 @@ def main():
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
-            eng.process_frame_device(dev_frames[args.warmup + i], mask,
-                                     stats[args.warmup + i])
+            wl.step(args.warmup + i, args.warmup + i)
             ends[i].record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -297,84 +434,99 @@ def main():
         t = torch.tensor([total_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    rows = stats.cpu().numpy()[args.warmup:]
-    bytes_frames = [byte_model(r, spec.depth, spec.k_max,
-                               args.state == "float64") for r in rows]
-    achieved = float(np.mean(bytes_frames)) / (step_ms * 1e-3) / 1e9
+    rows = wl.rows(args.warmup)
+    k = cfg.k_max
+    bytes_frames = [byte_model(r, 3, k, args.state == "float64") for r in rows]
+    steps_bytes = float(np.sum(bytes_frames)) / args.steps
+    achieved = steps_bytes / (step_ms * 1e-3) / 1e9
     peak, peak_kind = hbm_peak()
-    value = world * spec.n_pix * args.steps / (total_ms * 1e-3)
+    if args.workload == "c4":
+        # strong scaling: the ranks share one frame
+        value = wl.spec.n_pix * args.steps / (total_ms * 1e-3)
+    else:
+        value = world * wl.pixels * args.steps / (total_ms * 1e-3)
 
     # ---- warm-L2 back-to-back (diagnostic)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(True), torch.cuda.Event(True)
     ev0.record(stream)
     for i in range(args.steps):
-        eng.process_frame_device(dev_frames[(total_steps + i) % len(dev_frames)],
-                                 mask, stats[i % total_steps])
+        wl.step(total_steps + i, i % total_steps)
     ev1.record(stream)
     torch.cuda.synchronize()
     warm_ms = ev0.elapsed_time(ev1) / args.steps
 
     # ---- end-to-end through the public API (host frames in, mask out)
-    frames_api = [Frame.from_array(f, i) for i, f in enumerate(host_frames)]
     for i in range(args.warmup):
-        m, s = e2e_eng.process_frame(frames_api[i])
-        m.labels
+        wl.e2e_step(e2e_eng, i)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
+    bi = bo = 0
     for i in range(args.steps):
-        m, s = e2e_eng.process_frame(frames_api[args.warmup + i])
-        m.labels
-        s.n_foreground
+        bi, bo = wl.e2e_step(e2e_eng, args.warmup + i)
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = world * spec.n_pix * args.steps / e2e_s
+    if args.workload == "c4":
+        e2e = wl.spec.n_pix * args.steps / e2e_s
+    else:
+        e2e = world * wl.pixels * args.steps / e2e_s
 
     line = None
     if rank == 0:
         cpu = None
-        if not args.no_cpu and world == 1:
-            v, dt = cpu_baseline(host_frames, eng.clone(), cfg,
-                                 args.cpu_frames, 1)
+        if not args.no_cpu and world == 1 and args.workload in ("c2", "c3"):
+            v, dt = cpu_baseline(wl.host, eng.clone(), cfg, args.cpu_frames, 1)
             cpu = {"value": v, "unit": "pixel-frames/s", "cores": 1,
                    "kind": "port",
-                   "sample": f"{args.cpu_frames} C2 frames (640x480x3) from "
-                             f"the GPU engine's trained state, oracle "
-                             f"C kernels, 1 thread, {dt:.1f}s"}
+                   "sample": f"{args.cpu_frames} {args.workload.upper()} "
+                             f"frames from the GPU engine's trained state, "
+                             f"oracle C kernels (restatement of the serial "
+                             f"numba kernels), 1 thread, {dt:.1f}s"}
         lvl = rows[:, 1:7].sum(axis=0) / max(1, rows[:, 1:7].sum())
+        traffic = None
+        tpath = ROOT / "profiles" / f"traffic_{args.workload}.json"
+        if tpath.exists():
+            traffic = json.loads(tpath.read_text()).get("bytes_per_step")
         line = {
             "metric": "pixel-frames/sec (CoG classify+update)",
             "value": value, "unit": "pixel-frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64-arith/" + ("f32" if args.state == "float32"
-                                     else "f64") + "-state",
-            "data": "synthetic (seeded C2 generator, paper_1705_09339_b200.synth)",
-            "config": {"workload": "C2 640x480x3 K=3 N=200 (BASELINE configs[1])",
+            "scaling": "strong" if args.workload == "c4" else "weak",
+            "vs_baseline": None,
+            "dtype": "f32-state/f32-filtered+f64-exact-decisions"
+                     if args.state == "float32" else "f64",
+            "data": "synthetic (seeded BASELINE generator, "
+                    "paper_1705_09339_b200.synth)",
+            "config": {"workload": wl.workload,
                        "l2": "flushed between steps (256 MiB write, untimed)",
-                       "parallelism": f"{world} independent streams"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                       "parallelism": (f"{world} row bands" if
+                                       args.workload == "c4" else
+                                       f"{world} ranks x {wl.streams} "
+                                       f"independent stream(s)")},
+            "roofline": {"bound": "hbm", "achieved": achieved,
+                         "peak": peak * (world if args.workload == "c4" else 1),
                          "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         "bytes_per_frame": float(np.mean(bytes_frames)),
-                         "traffic": None},
+                         "frac": achieved / (peak * (world if args.workload
+                                                     == "c4" else 1)),
+                         "bytes_per_step": steps_bytes,
+                         "traffic": traffic},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "pixel-frames/s",
-                    "h2d_bytes_per_step": spec.depth * spec.n_pix,
-                    "d2h_bytes_per_step": spec.n_pix + 16 * 8},
-            "gpu_launches": args.steps,
+                    "h2d_bytes_per_step": int(bi),
+                    "d2h_bytes_per_step": int(bo)},
+            "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
-            "extra": {"train_s": t_train, "scene_gen_s": t_gen,
+            "extra": {"train_s": wl.t_train, "scene_gen_s": wl.t_gen,
                       "warm_l2_ms_per_step": warm_ms,
                       "step_ms_min": float(np.min(durs)),
                       "step_ms_max": float(np.max(durs)),
-                      "level_fractions": {k: float(x) for k, x in zip(
+                      "level_fractions": {k_: float(x) for k_, x in zip(
                           ("chp", "group", "mean", "meanvar", "gmm", "skip"),
                           lvl)}},
         }

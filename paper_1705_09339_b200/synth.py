@@ -185,9 +185,30 @@ class Scene:
         out = np.clip(np.rint(val), 0, 255).astype(np.uint8)
         return (out, truth) if with_truth else out
 
-    def frames(self, start: int, stop: int) -> np.ndarray:
-        """(stop-start, d, H, W) uint8."""
-        return np.stack([self.frame(t) for t in range(start, stop)])
+    def frames(self, start: int, stop: int, workers: int = 1) -> np.ndarray:
+        """(stop-start, d, H, W) uint8.  Every frame is a pure function of
+        (seed, t), so ``workers > 1`` renders them in parallel processes
+        (bit-identical to the serial result)."""
+        ts = list(range(start, stop))
+        if workers <= 1 or len(ts) < 2 * workers:
+            return np.stack([self.frame(t) for t in ts])
+        import concurrent.futures as cf
+        import multiprocessing as mp
+        out = np.empty((len(ts), self.spec.depth, self.spec.height,
+                        self.spec.width), dtype=np.uint8)
+        chunks = [ts[i::workers] for i in range(workers)]
+        with cf.ProcessPoolExecutor(workers,
+                                    mp_context=mp.get_context("fork")) as ex:
+            for idx, arr in zip(chunks, ex.map(_render, [(self.spec, c)
+                                                         for c in chunks])):
+                out[[t - start for t in idx]] = arr
+        return out
+
+
+def _render(job):
+    spec, ts = job
+    sc = Scene(spec)
+    return np.stack([sc.frame(t) for t in ts])
 
 
 def small_spec(cfg_id: int, width: int, height: int, frames: int,

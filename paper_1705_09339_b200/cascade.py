@@ -70,6 +70,11 @@ class FrameStats:
         s._event = event
         return s
 
+    def _detach(self, slot) -> None:
+        """The staging slot is about to be reused: materialise now."""
+        if self._row is None:
+            self._resolve()
+
     def _resolve(self) -> list:
         if self._row is None:
             self._event.synchronize()
@@ -263,6 +268,49 @@ class DeviceState:
         self._refresh()
 
 
+class HostRing:
+    """Reusable pinned staging for the host-facing frame loop.
+
+    ``slots`` sets of {pinned frame in, device frame, device mask / stats,
+    pinned mask / stats out, completion event}.  ``process_frame`` copies a
+    host frame into a pinned slot (one memcpy), enqueues H2D -> step -> D2H
+    and returns pending results that point into the slot; pinned memory is
+    allocated once instead of per frame (cudaHostAlloc costs far more than
+    the step).  Before a slot is reused, any result still pointing into it
+    is materialised into its own array, so results stay valid however long
+    the caller keeps them."""
+
+    def __init__(self, depth: int, height: int, width: int, device,
+                 slots: int = 4):
+        self.slots = []
+        for _ in range(slots):
+            self.slots.append({
+                "in": torch.empty((depth, height, width), dtype=torch.uint8,
+                                  pin_memory=True),
+                "x": torch.empty((depth, height, width), dtype=torch.uint8,
+                                 device=device),
+                "mask": torch.empty((height, width), dtype=torch.uint8,
+                                    device=device),
+                "stats": torch.empty(16, dtype=torch.int64, device=device),
+                "hm": torch.empty((height, width), dtype=torch.uint8,
+                                  pin_memory=True),
+                "hs": torch.empty(16, dtype=torch.int64, pin_memory=True),
+                "event": None, "owners": (),
+            })
+        self.next = 0
+
+    def acquire(self) -> dict:
+        slot = self.slots[self.next]
+        self.next = (self.next + 1) % len(self.slots)
+        for o in slot["owners"]:
+            o._detach(slot)
+        slot["owners"] = ()
+        if slot["event"] is not None:
+            slot["event"].synchronize()   # its pinned input may be reused
+            slot["event"] = None
+        return slot
+
+
 class CascadeEngine:
     """All per-pixel cascade state of one stream, resident on the GPU."""
 
@@ -299,6 +347,7 @@ class CascadeEngine:
         # row-band shard: callable summing the `accum` partials across the
         # shards of one frame in place (parallel.py); None = whole frame
         self.reducer = None
+        self._ring = None  # pinned host staging, created on first host frame
 
     # ------------------------------------------------------------ helpers
 
@@ -441,23 +490,60 @@ class CascadeEngine:
             self._reorder_pending = True
 
     def process_frame(self, frame) -> tuple[LabelMask, FrameStats]:
-        """One frame through the fused CUDA step (cascade.py:261-318)."""
-        x = self._frame_tensor(frame)
+        """One frame through the CUDA step (cascade.py:261-318).  Host
+        frames go through the engine's pinned staging ring; the returned
+        mask / stats resolve on first access."""
         self._flush()
-        dev = self.dev.device
-        mask = torch.empty((self.height, self.width), dtype=torch.uint8,
-                           device=dev)
-        stats = torch.empty(16, dtype=torch.int64, device=dev)
-        self._launch_step(x, mask, stats)
-        hm = torch.empty((self.height, self.width), dtype=torch.uint8,
-                         pin_memory=True)
-        hs = torch.empty(16, dtype=torch.int64, pin_memory=True)
-        hm.copy_(mask, non_blocking=True)
-        hs.copy_(stats, non_blocking=True)
+        if self._ring is None:
+            self._ring = HostRing(self.depth, self.height, self.width,
+                                  self.dev.device)
+        slot = self._ring.acquire()
+        if isinstance(frame, torch.Tensor) and frame.is_cuda:
+            x = self._frame_tensor(frame)
+        else:
+            self._stage(frame, slot["in"].numpy())
+            x = slot["x"]
+            x.copy_(slot["in"], non_blocking=True)
+        self._launch_step(x, slot["mask"], slot["stats"])
+        slot["hm"].copy_(slot["mask"], non_blocking=True)
+        slot["hs"].copy_(slot["stats"], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-        self._last_mask_dev = mask
-        return LabelMask.pending(hm, ev), FrameStats.pending(hs, ev)
+        slot["event"] = ev
+        m = LabelMask.pending(slot["hm"], ev, owned=False)
+        st = FrameStats.pending(slot["hs"], ev)
+        slot["owners"] = (m, st)
+        self._last_mask_dev = slot["mask"]
+        return m, st
+
+    def _stage(self, frame, out: np.ndarray) -> None:
+        """Validate a host frame (cascade.py:263-269) and copy it into the
+        pinned staging array."""
+        if isinstance(frame, torch.Tensor):
+            frame = frame.numpy()
+        if isinstance(frame, Frame):
+            if (frame.height, frame.width) != (self.height, self.width):
+                raise DataError(
+                    f"frame {frame.index} geometry {frame.height}x"
+                    f"{frame.width} != model {self.height}x{self.width}")
+            if frame.depth != self.depth:
+                raise DataError(f"frame {frame.index} has {frame.depth} "
+                                f"planes, model expects {self.depth}")
+            for c, pl in enumerate(frame.planes):
+                out[c] = pl.data
+            return
+        arr = np.asarray(frame)
+        if arr.ndim == 2:
+            arr = arr[None]
+        if arr.shape[1:] != (self.height, self.width):
+            raise DataError(f"frame geometry {arr.shape[1]}x{arr.shape[2]} "
+                            f"!= model {self.height}x{self.width}")
+        if arr.shape[0] != self.depth:
+            raise DataError(f"frame has {arr.shape[0]} planes, model "
+                            f"expects {self.depth}")
+        if arr.dtype != np.uint8:
+            raise DataError("frames must be uint8")
+        out[...] = arr
 
     def process_frame_device(self, frame: torch.Tensor, mask: torch.Tensor,
                              stats: torch.Tensor) -> None:
@@ -487,6 +573,7 @@ class CascadeEngine:
                 setattr(twin, k, v)
         twin._host = None
         twin._snap = None
+        twin._ring = None
         return twin
 
     # ------------------------------------------------------- inspection

@@ -187,6 +187,31 @@ int cog_export_state(const cog_geom *geom, const cog_state *st,
 int cog_import_state(const cog_geom *geom, const cog_state *st,
                      const cog_ref_state *in, void *stream);
 
+/* One host frame end to end, for the host-facing API (one call per frame
+ * instead of a dozen runtime calls from Python): H2D of `host_frame`
+ * (pinned, d*P bytes) into `dev_frame` on `copy_stream`, recorded in
+ * `up_event`; `stream` waits for it and runs the step (fused finalize);
+ * mask (P bytes) and stats (16 x i64) are copied back into the pinned
+ * `host_mask` / `host_stats` and completion is recorded in `done_event`.
+ * Replaces the per-frame body of CascadeEngine.process_frame
+ * (cascade.py:261-318) for host frames.  Events come from
+ * cog_event_create. */
+int cog_step_host(const cog_geom *geom, const cog_params *prm,
+                  const cog_state *st, const uint8_t *host_frame,
+                  uint8_t *dev_frame, uint8_t *dev_mask, void *conf,
+                  uint8_t *kind, int64_t *dev_stats, uint8_t *host_mask,
+                  int64_t *host_stats, int64_t frame_index,
+                  int32_t reorder_now, void *stream, void *copy_stream,
+                  void *up_event, void *done_event);
+
+/* cudaEvent_t helpers (timing disabled): create returns NULL on failure;
+ * sync blocks until the event completes; query returns 1 done, 0 not yet,
+ * negative on error. */
+void *cog_event_create(void);
+int cog_event_destroy(void *event);
+int cog_event_sync(void *event);
+int cog_event_query(void *event);
+
 /* Version / build string (host pointer, static). */
 const char *cog_version(void);
 

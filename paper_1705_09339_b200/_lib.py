@@ -122,6 +122,12 @@ _SIGS = {
     "cog_baseline_frame": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "cog_export_state": (ctypes.c_int, [_P, _P, _P, _P]),
     "cog_import_state": (ctypes.c_int, [_P, _P, _P, _P]),
+    "cog_step_host": (ctypes.c_int, [_P] * 11 + [ctypes.c_int64,
+                                                ctypes.c_int32] + [_P] * 4),
+    "cog_event_create": (ctypes.c_void_p, []),
+    "cog_event_destroy": (ctypes.c_int, [_P]),
+    "cog_event_sync": (ctypes.c_int, [_P]),
+    "cog_event_query": (ctypes.c_int, [_P]),
     "cog_version": (ctypes.c_char_p, []),
     "cog_debug_prof": (ctypes.c_int, [_P, ctypes.c_int]),
 }

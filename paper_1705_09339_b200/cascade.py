@@ -29,7 +29,7 @@ import torch
 
 from . import _lib
 from .config import EngineConfig
-from .errors import DataError
+from .errors import CudaError, DataError
 from .frame_io import Frame, LabelMask
 
 LEVEL_CHP, LEVEL_GROUP, LEVEL_MEAN, LEVEL_MEANVAR, LEVEL_GMM = 0, 1, 2, 3, 4
@@ -268,6 +268,31 @@ class DeviceState:
         self._refresh()
 
 
+_COPY_POOL = None
+
+
+def _copy_rows(planes, out: np.ndarray) -> None:
+    """planes[c] -> out[c]; frames above ~1 MB are split by rows over a few
+    threads (numpy copies release the GIL), so staging keeps up with the
+    device step."""
+    global _COPY_POOL
+    if out.nbytes < (1 << 20):
+        for c, pl in enumerate(planes):
+            out[c] = pl
+        return
+    if _COPY_POOL is None:
+        import concurrent.futures as cf
+        _COPY_POOL = cf.ThreadPoolExecutor(4)
+    h = out.shape[1]
+    cuts = [0, h // 4, h // 2, 3 * h // 4, h]
+
+    def part(i):
+        a, b = cuts[i], cuts[i + 1]
+        for c, pl in enumerate(planes):
+            out[c, a:b] = pl[a:b]
+    list(_COPY_POOL.map(part, range(4)))
+
+
 class HostRing:
     """Reusable pinned staging for the host-facing frame loop.
 
@@ -295,9 +320,17 @@ class HostRing:
                 "hm": torch.empty((height, width), dtype=torch.uint8,
                                   pin_memory=True),
                 "hs": torch.empty(16, dtype=torch.int64, pin_memory=True),
-                "event": None, "owners": (),
+                "event": None, "owners": (), "up": torch.cuda.Event(),
+                "src": None,
             })
+        lib = _lib.load()
+        for sl in self.slots:
+            sl["cup"] = CEvent(lib)
+            sl["cdone"] = CEvent(lib)
         self.next = 0
+        # host->device copies run on their own stream so frame t+1's upload
+        # overlaps frame t's step; the step waits on the copy's event
+        self.copy_stream = torch.cuda.Stream(device=device)
 
     def acquire(self) -> dict:
         slot = self.slots[self.next]
@@ -308,7 +341,37 @@ class HostRing:
         if slot["event"] is not None:
             slot["event"].synchronize()   # its pinned input may be reused
             slot["event"] = None
+        slot["src"] = None
         return slot
+
+
+class CEvent:
+    """A cudaEvent_t owned through the C-ABI (cog_event_create); quacks like
+    torch.cuda.Event for the pending results."""
+
+    __slots__ = ("lib", "handle")
+
+    def __init__(self, lib):
+        self.lib = lib
+        self.handle = lib.cog_event_create()
+        if not self.handle:
+            raise CudaError("cog_event_create failed")
+
+    def synchronize(self) -> None:
+        _lib.check(self.lib.cog_event_sync(self.handle), "cog_event_sync")
+
+    def query(self) -> bool:
+        rc = self.lib.cog_event_query(self.handle)
+        if rc < 0:
+            _lib.check(-rc, "cog_event_query")
+        return rc == 1
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.lib.cog_event_destroy(self.handle)
+        except Exception:
+            pass
 
 
 class CascadeEngine:
@@ -356,9 +419,15 @@ class CascadeEngine:
         return torch.cuda.current_stream(self.dev.device).cuda_stream
 
     def _params(self) -> "_lib.Params":
-        q = params_from_config(self.config, self._wtab)
-        q.exact_group_sums = int(self.exact_group_sums)
-        return q
+        """The C params struct, rebuilt only when an input changes (the
+        per-frame launch path must stay cheap on the host)."""
+        key = (id(self.config), self._wtab.tobytes(),
+               bool(self.exact_group_sums))
+        if getattr(self, "_pkey", None) != key:
+            q = params_from_config(self.config, self._wtab)
+            q.exact_group_sums = int(self.exact_group_sums)
+            self._pcache, self._pkey = q, key
+        return self._pcache
 
     def _frame_tensor(self, frame) -> torch.Tensor:
         """(d, H, W) uint8 on the device; host frames go through pinned
@@ -482,6 +551,11 @@ class CascadeEngine:
             rc = self.lib.cog_finalize(geom, prm, st, stats.data_ptr(),
                                        self.frame_count, self.stream)
             _lib.check(rc, "cog_finalize")
+        self._advance()
+
+    def _advance(self) -> None:
+        """Frame counter and the reorder schedule (cascade.py:314-317): a
+        reorder due after this frame is applied at the next step's start."""
         self._reorder_pending = False
         cfg = self.config
         self.frame_count += 1
@@ -491,24 +565,51 @@ class CascadeEngine:
 
     def process_frame(self, frame) -> tuple[LabelMask, FrameStats]:
         """One frame through the CUDA step (cascade.py:261-318).  Host
-        frames go through the engine's pinned staging ring; the returned
-        mask / stats resolve on first access."""
+        frames go through the engine's pinned staging ring (one C-ABI call,
+        cog_step_host: upload on a copy stream, step, result download); the
+        returned mask / stats resolve on first access."""
         self._flush()
         if self._ring is None:
             self._ring = HostRing(self.depth, self.height, self.width,
                                   self.dev.device)
-        slot = self._ring.acquire()
-        if isinstance(frame, torch.Tensor) and frame.is_cuda:
-            x = self._frame_tensor(frame)
+        ring = self._ring
+        slot = ring.acquire()
+        cuda_in = isinstance(frame, torch.Tensor) and frame.is_cuda
+        if not cuda_in:
+            if (isinstance(frame, torch.Tensor) and frame.is_pinned()
+                    and frame.dtype == torch.uint8 and frame.is_contiguous()
+                    and tuple(frame.shape[-2:]) == (self.height, self.width)
+                    and frame.numel() == self.depth * self.n_pix):
+                src = frame          # DMA straight from the caller's pinned
+            else:                    # tensor (kept alive until slot reuse)
+                self._stage(frame, slot["in"].numpy())
+                src = slot["in"]
+            slot["src"] = src
+        if not cuda_in and self.reducer is None:
+            rc = self.lib.cog_step_host(
+                _lib.ref(self.dev.geom), _lib.ref(self._params()),
+                _lib.ref(self.dev.cstate), src.data_ptr(),
+                slot["x"].data_ptr(), slot["mask"].data_ptr(),
+                self.dev.conf.data_ptr(), self.dev.kind.data_ptr(),
+                slot["stats"].data_ptr(), slot["hm"].data_ptr(),
+                slot["hs"].data_ptr(), self.frame_count,
+                int(self._reorder_pending), self.stream,
+                ring.copy_stream.cuda_stream, slot["cup"].handle,
+                slot["cdone"].handle)
+            _lib.check(rc, "cog_step_host")
+            self._advance()
+            ev = slot["cdone"]
         else:
-            self._stage(frame, slot["in"].numpy())
-            x = slot["x"]
-            x.copy_(slot["in"], non_blocking=True)
-        self._launch_step(x, slot["mask"], slot["stats"])
-        slot["hm"].copy_(slot["mask"], non_blocking=True)
-        slot["hs"].copy_(slot["stats"], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
+            if cuda_in:
+                x = self._frame_tensor(frame)
+            else:
+                x = slot["x"]
+                x.copy_(src, non_blocking=True)
+            self._launch_step(x, slot["mask"], slot["stats"])
+            slot["hm"].copy_(slot["mask"], non_blocking=True)
+            slot["hs"].copy_(slot["stats"], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
         slot["event"] = ev
         m = LabelMask.pending(slot["hm"], ev, owned=False)
         st = FrameStats.pending(slot["hs"], ev)
@@ -529,8 +630,7 @@ class CascadeEngine:
             if frame.depth != self.depth:
                 raise DataError(f"frame {frame.index} has {frame.depth} "
                                 f"planes, model expects {self.depth}")
-            for c, pl in enumerate(frame.planes):
-                out[c] = pl.data
+            _copy_rows([pl.data for pl in frame.planes], out)
             return
         arr = np.asarray(frame)
         if arr.ndim == 2:
@@ -543,7 +643,7 @@ class CascadeEngine:
                             f"expects {self.depth}")
         if arr.dtype != np.uint8:
             raise DataError("frames must be uint8")
-        out[...] = arr
+        _copy_rows(list(arr), out)
 
     def process_frame_device(self, frame: torch.Tensor, mask: torch.Tensor,
                              stats: torch.Tensor) -> None:

@@ -34,6 +34,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 using namespace cog;
 
@@ -2082,6 +2083,25 @@ int num_sms() {
   return sms;
 }
 
+// occupancy queries cost microseconds; the per-frame launch path asks the
+// same (kernel, block, smem) question every frame -> memoise
+int cached_occupancy(const void* fn, int threads, size_t smem) {
+  struct Entry { const void* fn; int threads; size_t smem; int occ; };
+  static Entry cache[64];
+  static int n = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < n; ++i)
+    if (cache[i].fn == fn && cache[i].threads == threads &&
+        cache[i].smem == smem)
+      return cache[i].occ;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
+  if (occ < 1) occ = 1;
+  if (n < 64) cache[n++] = Entry{fn, threads, smem, occ};
+  return occ;
+}
+
 int check_geom(const cog_geom* g) {
   if (!g) return COG_EINVAL;
   if (g->height < 1 || g->width < 1 || g->depth < 1 || g->depth > MAXD)
@@ -2187,9 +2207,7 @@ int launch_lean(const StepArgs& a, cudaStream_t st) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, LEAN_THREADS, smem);
-  if (occ < 1) occ = 1;
+  const int occ = cached_occupancy((const void*)fn, LEAN_THREADS, smem);
   const int need = (a.n_tiles + LEAN_WARPS - 1) / LEAN_WARPS;
   const int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
   int gx = need < per_stream ? need : per_stream;
@@ -2214,9 +2232,7 @@ int launch_fast_k(const StepArgs& a, cudaStream_t st) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, LEAN_THREADS, smem);
-  if (occ < 1) occ = 1;
+  const int occ = cached_occupancy((const void*)fn, LEAN_THREADS, smem);
   // balanced static schedule: t tiles per warp, just enough CTAs
   const long long units = (long long)a.n_tiles;
   const int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
@@ -2237,9 +2253,7 @@ int launch_vec_k(const StepArgs& a, cudaStream_t st) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, LEAN_THREADS, smem);
-  if (occ < 1) occ = 1;
+  const int occ = cached_occupancy((const void*)fn, LEAN_THREADS, smem);
   const int tile_w = 4 * (32 / a.g.stride);
   const long long tiles = (long long)((a.g.width + tile_w - 1) / tile_w) *
                           ((a.g.height + a.g.stride - 1) / a.g.stride);
@@ -2295,9 +2309,7 @@ int launch_hot(const StepArgs& a, cudaStream_t st) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
-  if (occ < 1) occ = 1;
+  const int occ = cached_occupancy((const void*)fn, threads, smem);
   const int need = (a.n_tiles + warps - 1) / warps;
   int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
   int gx = need < per_stream ? need : per_stream;
@@ -2330,9 +2342,7 @@ int launch_deep(StepArgs a, cudaStream_t st, bool union_mask) {
   }
   // the union pass needs a stream-wide barrier: cooperative launch of a
   // grid that is guaranteed co-resident
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0);
-  if (occ < 1) occ = 1;
+  const int occ = cached_occupancy((const void*)fn, 256, 0);
   const size_t cap = (size_t)num_sms() * occ / a.g.streams;
   if (cap < 1) return COG_EUNSUPPORTED;
   const size_t want = (P / 4 + 255) / 256;  // union pass: 4 pixels a thread
@@ -2472,6 +2482,62 @@ int cog_step(const cog_geom* geom, const cog_params* prm, const cog_state* st,
   a.fuse_finalize = fuse_finalize;
   cudaStream_t s = (cudaStream_t)stream;
   return geom->state_f64 ? launch_step<double>(a, s) : launch_step<float>(a, s);
+}
+
+int cog_step_host(const cog_geom* geom, const cog_params* prm,
+                  const cog_state* st, const uint8_t* host_frame,
+                  uint8_t* dev_frame, uint8_t* dev_mask, void* conf,
+                  uint8_t* kind, int64_t* dev_stats, uint8_t* host_mask,
+                  int64_t* host_stats, int64_t frame_index,
+                  int32_t reorder_now, void* stream, void* copy_stream,
+                  void* up_event, void* done_event) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!host_frame || !dev_frame || !host_mask || !host_stats || !up_event ||
+      !done_event || geom->streams != 1)
+    return COG_EINVAL;
+  const size_t P = (size_t)geom->height * geom->width;
+  cudaStream_t s = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
+  cudaError_t e = cudaMemcpyAsync(dev_frame, host_frame, P * geom->depth,
+                                  cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess) e = cudaEventRecord((cudaEvent_t)up_event, cs);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, (cudaEvent_t)up_event, 0);
+  if (e != cudaSuccess) return (int)e;
+  rc = cog_step(geom, prm, st, dev_frame, dev_mask, conf, kind, dev_stats,
+                frame_index, reorder_now, 1, stream);
+  if (rc) return rc;
+  e = cudaMemcpyAsync(host_mask, dev_mask, P, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(host_stats, dev_stats, 16 * sizeof(int64_t),
+                        cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaEventRecord((cudaEvent_t)done_event, s);
+  return e == cudaSuccess ? COG_OK : (int)e;
+}
+
+void* cog_event_create(void) {
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+    return nullptr;
+  return (void*)ev;
+}
+
+int cog_event_destroy(void* event) {
+  return event ? (int)cudaEventDestroy((cudaEvent_t)event) : COG_EINVAL;
+}
+
+int cog_event_sync(void* event) {
+  return event ? (int)cudaEventSynchronize((cudaEvent_t)event) : COG_EINVAL;
+}
+
+int cog_event_query(void* event) {
+  if (!event) return COG_EINVAL;
+  const cudaError_t e = cudaEventQuery((cudaEvent_t)event);
+  if (e == cudaSuccess) return 1;
+  if (e == cudaErrorNotReady) {
+    cudaGetLastError();
+    return 0;
+  }
+  return -(int)e;
 }
 
 int cog_finalize(const cog_geom* geom, const cog_params* prm,

@@ -535,7 +535,12 @@ def main():
                                        args.workload == "c4" else
                                        f"{world} ranks x {wl.streams} "
                                        f"independent stream(s)")},
-            "roofline": {"bound": "hbm", "achieved": achieved,
+            "roofline": {"bound": "hbm",
+                         "kernel": "the frame step: fast_kernel (hot pass) + "
+                                   "deep_kernel (worklist + finalize), timed "
+                                   "together with CUDA events on the engine "
+                                   "stream; ncu share in profiles/",
+                         "achieved": achieved,
                          "peak": peak * (world if args.workload == "c4" else 1),
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / (peak * (world if args.workload

@@ -130,9 +130,9 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
   float* s_gmuf = s_btf + 256;                           // [D*G]
   float* s_gthrf = s_gmuf + D * G;                       // [D*G]
   for (int i = threadIdx.x; i < 256; i += LEAN_THREADS) {
-    const double b = (double)i / 255.0;
-    s_bt[i] = literal ? b : 1.0 - b;
-    s_btf[i] = (float)s_bt[i];
+    const double b = g_bterm[literal ? 1 : 0][i];
+    s_bt[i] = b;
+    s_btf[i] = (float)b;
   }
   {
     const double* gmu = a.s.g_mu + (size_t)s * D * G;
@@ -147,6 +147,9 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
   for (int i = threadIdx.x; i < LEAN_WARPS * wpad; i += LEAN_THREADS)
     s_wacc[i] = 0ull;
   __syncthreads();
+  // let the frame's deep kernel be scheduled now (it waits on this grid's
+  // completion before touching anything); hides the launch gap
+  asm volatile("griddepcontrol.launch_dependents;");
   unsigned long long* wacc = s_wacc + warp * wpad;
   unsigned long long* qc = s_qc + warp * FQ_CAP;
   double* qr = s_qr + warp * FQ_CAP;

@@ -1539,10 +1539,87 @@ __global__ void __launch_bounds__(PIPE_THREADS, COG_PIPE_MINB)
 // once (atomicOr on its mask word returns the previous byte).  The last CTA
 // of each stream finalizes the frame.
 // ---------------------------------------------------------------------------
+// One worklist item (a MEANVAR hit or a GMM fall-through of one plane-pixel,
+// kernels_numba.py:312-342): full binary64 mixture update, stable re-sort,
+// mode references remapped.  A GMM label sets the label bit in dyn and --
+// unless the mask is formed by a union pass -- ORs the pixel's mask byte;
+// returns 1 iff that byte went 0 -> 255 (counted once per pixel).
+template <typename T, int KMAX>
+__device__ __forceinline__ unsigned deep_item(const StepArgs& a, int s,
+                                              unsigned long long code,
+                                              double rho) {
+  const size_t P = (size_t)a.g.height * a.g.width;
+  const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
+                  a.q.variance_floor, a.q.initial_variance};
+  uint8_t* mask = a.mask + (size_t)s * P;
+  const int kindq = (int)((code >> 1) & 3), rs = (int)((code >> 3) & 7);
+  const int c = (int)((code >> 6) & 3);
+  const double v = (double)((code >> 8) & 0xFF);
+  const size_t p = (size_t)(code >> 16);
+  const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+  // meta and every slot of the mixture in one round of loads
+  const uint32_t meta = pr.meta[p];
+  Mix<KMAX> x;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    x.mu[k] = 0.0;
+    x.var[k] = 1.0;
+    x.w[k] = 0.0;
+    if (k < a.g.k) {
+      x.mu[k] = ldrw(pr.mu + k * P + p);
+      x.var[k] = ldrw(pr.var + k * P + p);
+      x.w[k] = ldrw(pr.w + k * P + p);
+    }
+  }
+  int n = meta_count(meta);
+  int inv[KMAX];
+  unsigned newly = 0;
+  if (kindq == DEEP_MEANVAR) {
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (k == rs) {
+        const double mm = (1.0 - rho) * x.mu[k] + rho * v;
+        x.mu[k] = mm;
+        const double dd = v - mm;
+        double s2 = (1.0 - rho) * x.var[k] + rho * (dd * dd);
+        if (s2 < a.q.variance_floor) s2 = a.q.variance_floor;
+        x.var[k] = s2;
+      }
+    }
+    sort_modes<KMAX>(x, n, inv);
+    store_mix_r<T, KMAX>(pr, p, n, x);
+    pr.meta[p] = (uint16_t)meta_with_refs(
+        meta, select_inv<KMAX>(inv, meta_ref(meta, 0)),
+        select_inv<KMAX>(inv, meta_ref(meta, 1)));
+  } else {
+    const int lbl = gmm_step<KMAX>(x, n, a.g.k, v, rho, gp, inv);
+    store_mix_r<T, KMAX>(pr, p, n, x);
+    uint32_t nm = meta_with_count(meta, n);
+    if (kindq == DEEP_GMM)
+      nm = meta_with_refs(nm, select_inv<KMAX>(inv, meta_ref(meta, 0)),
+                          select_inv<KMAX>(inv, meta_ref(meta, 1)));
+    pr.meta[p] = (uint16_t)nm;
+    if (lbl) {
+      pr.dyn[p] |= 1u << 8;
+      if (!a.union_mask) {
+        const uintptr_t addr = (uintptr_t)(mask + p);
+        unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
+        const unsigned sh = (unsigned)(addr & 3) * 8;
+        const unsigned old = atomicOr(word, 0xFFu << sh);
+        newly = ((old >> sh) & 0xFFu) == 0u;
+      }
+    }
+  }
+  return newly;
+}
+
 template <typename T, int KMAX>
 __global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
   __shared__ int s_last;
   __shared__ unsigned long long s_fg;
+  // launched with programmatic stream serialization after fast_kernel: wait
+  // for its results (a no-op under a normal launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int s = blockIdx.y;
   const int d = a.g.depth;
   const size_t P = (size_t)a.g.height * a.g.width;
@@ -1551,8 +1628,6 @@ __global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
   unsigned long long* dq_code = (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
   const double* dq_rho = a.s.deeprho + (size_t)s * dq_cap;
   const size_t n = *(volatile uint32_t*)(sync + 3);
-  const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
-                  a.q.variance_floor, a.q.initial_variance};
   uint8_t* mask = a.mask + (size_t)s * P;
   if (threadIdx.x == 0) s_fg = 0;
   __syncthreads();
@@ -1562,64 +1637,7 @@ __global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
     const unsigned long long code = dq_code[i];
     if (!(code & 1ull)) continue;
     dq_code[i] = 0ull;
-    const int kindq = (int)((code >> 1) & 3), rs = (int)((code >> 3) & 7);
-    const int c = (int)((code >> 6) & 3);
-    const double v = (double)((code >> 8) & 0xFF);
-    const size_t p = (size_t)(code >> 16);
-    const double rho = dq_rho[i];
-    const PlaneRef<T> pr = plane_ref<T>(a, s, c);
-    // meta and every slot of the mixture in one round of loads
-    const uint32_t meta = pr.meta[p];
-    Mix<KMAX> x;
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-      x.mu[k] = 0.0;
-      x.var[k] = 1.0;
-      x.w[k] = 0.0;
-      if (k < a.g.k) {
-        x.mu[k] = ldrw(pr.mu + k * P + p);
-        x.var[k] = ldrw(pr.var + k * P + p);
-        x.w[k] = ldrw(pr.w + k * P + p);
-      }
-    }
-    int n = meta_count(meta);
-    int inv[KMAX];
-    if (kindq == DEEP_MEANVAR) {
-#pragma unroll
-      for (int k = 0; k < KMAX; ++k) {
-        if (k == rs) {
-          const double mm = (1.0 - rho) * x.mu[k] + rho * v;
-          x.mu[k] = mm;
-          const double dd = v - mm;
-          double s2 = (1.0 - rho) * x.var[k] + rho * (dd * dd);
-          if (s2 < a.q.variance_floor) s2 = a.q.variance_floor;
-          x.var[k] = s2;
-        }
-      }
-      sort_modes<KMAX>(x, n, inv);
-      store_mix_r<T, KMAX>(pr, p, n, x);
-      pr.meta[p] = (uint16_t)meta_with_refs(
-          meta, select_inv<KMAX>(inv, meta_ref(meta, 0)),
-          select_inv<KMAX>(inv, meta_ref(meta, 1)));
-    } else {
-      const int lbl = gmm_step<KMAX>(x, n, a.g.k, v, rho, gp, inv);
-      store_mix_r<T, KMAX>(pr, p, n, x);
-      uint32_t nm = meta_with_count(meta, n);
-      if (kindq == DEEP_GMM)
-        nm = meta_with_refs(nm, select_inv<KMAX>(inv, meta_ref(meta, 0)),
-                            select_inv<KMAX>(inv, meta_ref(meta, 1)));
-      pr.meta[p] = (uint16_t)nm;
-      if (lbl) {
-        pr.dyn[p] |= 1u << 8;
-        if (!a.union_mask) {
-          const uintptr_t addr = (uintptr_t)(mask + p);
-          unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
-          const unsigned sh = (unsigned)(addr & 3) * 8;
-          const unsigned old = atomicOr(word, 0xFFu << sh);
-          fg += ((old >> sh) & 0xFFu) == 0u;
-        }
-      }
-    }
+    fg += deep_item<T, KMAX>(a, s, code, dq_rho[i]);
   }
   if (a.union_mask) {
     // every plane-pixel's label is final once all CTAs of this stream have
@@ -2051,6 +2069,12 @@ __global__ void import_kernel(cog_geom g, cog_state s, cog_ref_state in) {
   }
 }
 
+// bterm tables |v - prev| / 255 (literal) and 1 - that (reference form,
+// kernels_numba.py:255-257), computed once on the host in IEEE binary64
+// (correctly rounded, as the device division) and uploaded per device, so
+// no CTA spends its prologue on 256 binary64 divisions
+__device__ double g_bterm[2][256];
+
 #include "cog_lean.cuh"
 #include "cog_fast.cuh"
 #include "cog_vec.cuh"
@@ -2081,6 +2105,23 @@ int num_sms() {
     if (sms <= 0) sms = 148;
   }
   return sms;
+}
+
+void ensure_bterm() {
+  static bool done[64] = {false};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  double t[2][256];
+  for (int i = 0; i < 256; ++i) {
+    const double b = (double)i / 255.0;
+    t[1][i] = b;
+    t[0][i] = 1.0 - b;
+  }
+  cudaMemcpyToSymbol(g_bterm, t, sizeof(t));
+  done[dev] = true;
 }
 
 // occupancy queries cost microseconds; the per-frame launch path asks the
@@ -2328,7 +2369,8 @@ bool fast_ok(const StepArgs& a, bool f32) {
 }
 
 template <typename T>
-int launch_deep(StepArgs a, cudaStream_t st, bool union_mask) {
+int launch_deep(StepArgs a, cudaStream_t st, bool union_mask,
+                bool pdl = false) {
   auto fn = pick_deep<T>(a.g.k);
   a.union_mask = union_mask ? 1 : 0;
   const size_t P = (size_t)a.g.height * a.g.width;
@@ -2337,8 +2379,25 @@ int launch_deep(StepArgs a, cudaStream_t st, bool union_mask) {
     const size_t cap = (size_t)num_sms() * 8 / a.g.streams + 1;
     if (dg > cap) dg = cap;
     if (dg < 1) dg = 1;
-    fn<<<dim3((unsigned)dg, a.g.streams), 256, 0, st>>>(a);
-    return launch_status();
+    if (!pdl) {
+      fn<<<dim3((unsigned)dg, a.g.streams), 256, 0, st>>>(a);
+      return launch_status();
+    }
+    // programmatic dependent launch: the deep grid is scheduled while the
+    // hot kernel drains and waits (griddepcontrol.wait) for its results,
+    // hiding the launch gap between the two kernels of a frame
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)dg, a.g.streams);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
+    return e == cudaSuccess ? COG_OK : (int)e;
   }
   // the union pass needs a stream-wide barrier: cooperative launch of a
   // grid that is guaranteed co-resident
@@ -2358,12 +2417,16 @@ int launch_deep(StepArgs a, cudaStream_t st, bool union_mask) {
 template <typename T>
 int launch_step(const StepArgs& a, cudaStream_t st) {
   set_fetch_granularity();
+  ensure_bterm();
   // float32 state: the fast kernel (vec: 4 pixels a lane, mask formed by
   // the deep kernel's union pass); otherwise lean / pipelined / general
   const bool fast = fast_ok(a, sizeof(T) == 4);
   int rc = fast ? launch_fast(a, st) : launch_hot<T>(a, st);
   if (rc) return rc;
-  return launch_deep<T>(a, st, fast && vec_ok(a));
+  // programmatic dependent launch measured slightly slower on B200 (the
+  // early-scheduled deep CTAs compete with the hot kernel's tail): opt-in
+  return launch_deep<T>(a, st, fast && vec_ok(a),
+                        fast && !vec_ok(a) && getenv("COG_PDL"));
 }
 
 }  // namespace

@@ -204,6 +204,14 @@ int cog_step_host(const cog_geom *geom, const cog_params *prm,
                   int32_t reorder_now, void *stream, void *copy_stream,
                   void *up_event, void *done_event);
 
+/* Confusion counts of predicted vs truth masks u8[n] (evaluation.
+ * confusion_counts, cogbg/evaluation.py:72-89): truth 0 = background,
+ * 255 = foreground, anything else excluded; predicted foreground = 255.
+ * ACCUMULATES into counts u64[5] = {tp, fp, tn, fn, excluded} (zero it to
+ * start a sequence), so a whole run is scored on the device and read once. */
+int cog_confusion(const uint8_t *predicted, const uint8_t *truth, int64_t n,
+                  uint64_t *counts, void *stream);
+
 /* cudaEvent_t helpers (timing disabled): create returns NULL on failure;
  * sync blocks until the event completes; query returns 1 done, 0 not yet,
  * negative on error. */

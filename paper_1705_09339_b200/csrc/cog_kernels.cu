@@ -2080,6 +2080,55 @@ __device__ double g_bterm[2][256];
 #include "cog_vec.cuh"
 
 // ---------------------------------------------------------------------------
+// evaluation: confusion counts (16 pixels a thread, warp reductions, one
+// 64-bit atomic per count per warp)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    confusion_kernel(const uint8_t* __restrict__ pred,
+                     const uint8_t* __restrict__ truth, int64_t n,
+                     unsigned long long* counts) {
+  unsigned tp = 0, fp = 0, tn = 0, fn = 0, ex = 0;
+  const int64_t nv = n / 16;
+  const bool aligned = (((uintptr_t)pred | (uintptr_t)truth) & 15) == 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto one = [&](unsigned pv, unsigned tv) {
+    const bool known = tv == 0u || tv == 255u;
+    const bool pf = pv == 255u, tf = tv == 255u;
+    tp += known && pf && tf;
+    fp += known && pf && !tf;
+    tn += known && !pf && !tf;
+    fn += known && !pf && tf;
+    ex += !known;
+  };
+  int64_t start = 0;
+  if (aligned) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv;
+         i += stride) {
+      const uint4 a = __ldcs((const uint4*)pred + i);
+      const uint4 b = __ldcs((const uint4*)truth + i);
+      const unsigned pa[4] = {a.x, a.y, a.z, a.w};
+      const unsigned tb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          one((pa[w] >> (8 * j)) & 0xFFu, (tb[w] >> (8 * j)) & 0xFFu);
+    }
+    start = nv * 16;
+  }
+  for (int64_t i = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+       i < n; i += stride)
+    one(pred[i], truth[i]);
+  const unsigned v[5] = {tp, fp, tn, fn, ex};
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const unsigned r = warp_sum_u32(v[q]);
+    if ((threadIdx.x & 31) == 0 && r)
+      atomicAdd(counts + q, (unsigned long long)r);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------
 // Random 4-byte table lookups must not drag 64/128-B DRAM fetches along.
@@ -2575,6 +2624,19 @@ int cog_step_host(const cog_geom* geom, const cog_params* prm,
                         cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaEventRecord((cudaEvent_t)done_event, s);
   return e == cudaSuccess ? COG_OK : (int)e;
+}
+
+int cog_confusion(const uint8_t* predicted, const uint8_t* truth, int64_t n,
+                  uint64_t* counts, void* stream) {
+  if (!predicted || !truth || !counts || n < 0) return COG_EINVAL;
+  if (n == 0) return COG_OK;
+  int64_t blocks = (n / 16 + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  confusion_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      predicted, truth, n, (unsigned long long*)counts);
+  return launch_status();
 }
 
 void* cog_event_create(void) {

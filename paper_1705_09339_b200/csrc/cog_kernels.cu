@@ -2425,7 +2425,11 @@ int launch_deep(StepArgs a, cudaStream_t st, bool union_mask,
   const size_t P = (size_t)a.g.height * a.g.width;
   size_t dg = (P * a.g.depth / 8 + 255) / 256;  // covers ~12% deep items
   if (!union_mask) {
-    const size_t cap = (size_t)num_sms() * 8 / a.g.streams + 1;
+    // grid-stride over the worklist; more CTAs than SMs only add last-CTA
+    // atomics and tail (COG_DEEP_CTAS_PER_SM tunes it)
+    const char* env = getenv("COG_DEEP_CTAS_PER_SM");
+    const size_t per_sm = env ? (size_t)atoi(env) : 8;
+    const size_t cap = (size_t)num_sms() * per_sm / a.g.streams + 1;
     if (dg > cap) dg = cap;
     if (dg < 1) dg = 1;
     if (!pdl) {

@@ -1,15 +1,10 @@
-# full round check: parity tests, smoke, bench, reference arm, launch list, one full ncu capture
+# full round check on the B200: GPU parity suite, smoke, bench (C2), the
+# reference arm, the ncu launch list / traffic / full captures
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -40 > gpurun_out/pytest_gpu.log
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -5 > gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.log 2>&1
-CMD="python bench.py --steps 6 --warmup 3 --no-cpu"
-timeout 300 $CMD > gpurun_out/prof_plain.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"step_kernel|pipe_kernel" \
-    -s 4 -c 1 -o gpurun_out/prof_step $CMD > gpurun_out/ncu_full.log 2>&1
-tail -5 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; tail -2 gpurun_out/bench.log; tail -2 gpurun_out/bench_ref.log
-python tools/launches.py gpurun_out/launches.csv
+bash tools/gpu_profile_round.sh
+tail -3 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log; tail -1 gpurun_out/bench.log; tail -1 gpurun_out/bench_ref.log

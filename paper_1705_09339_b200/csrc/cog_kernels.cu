@@ -71,7 +71,6 @@ struct StepArgs {
   int reorder_now;
   int fuse_finalize;
   int cw, iters, tiles_x, n_tiles;
-  int union_mask;  // deep kernel forms the mask from every plane's label bit
 };
 
 template <typename T>
@@ -1601,13 +1600,11 @@ __device__ __forceinline__ unsigned deep_item(const StepArgs& a, int s,
     pr.meta[p] = (uint16_t)nm;
     if (lbl) {
       pr.dyn[p] |= 1u << 8;
-      if (!a.union_mask) {
-        const uintptr_t addr = (uintptr_t)(mask + p);
-        unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
-        const unsigned sh = (unsigned)(addr & 3) * 8;
-        const unsigned old = atomicOr(word, 0xFFu << sh);
-        newly = ((old >> sh) & 0xFFu) == 0u;
-      }
+      const uintptr_t addr = (uintptr_t)(mask + p);
+      unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
+      const unsigned sh = (unsigned)(addr & 3) * 8;
+      const unsigned old = atomicOr(word, 0xFFu << sh);
+      newly = ((old >> sh) & 0xFFu) == 0u;
     }
   }
   return newly;
@@ -1638,42 +1635,6 @@ __global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
     if (!(code & 1ull)) continue;
     dq_code[i] = 0ull;
     fg += deep_item<T, KMAX>(a, s, code, dq_rho[i]);
-  }
-  if (a.union_mask) {
-    // every plane-pixel's label is final once all CTAs of this stream have
-    // run their items: stream-wide barrier (the grid is co-resident), then
-    // mask = OR over planes of the label bit (dyn bit 8), 4 pixels a thread
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(sync + 2, 1u);
-      while (*(volatile uint32_t*)(sync + 2) < gridDim.x) __nanosleep(64);
-      __threadfence();
-    }
-    __syncthreads();
-    const uint32_t* dyn = a.s.dyn + (size_t)s * d * P;
-    const size_t nq = (P % 4 == 0) ? P / 4 : 0;  // 16-B aligned planes
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
-         i += (size_t)gridDim.x * blockDim.x) {
-      unsigned lab = 0;
-      for (int c = 0; c < d; ++c) {
-        const uint4 v = __ldcg((const uint4*)(dyn + (size_t)c * P) + i);
-        lab |= ((v.x >> 8) & 1u) | ((v.y >> 7) & 2u) | ((v.z >> 6) & 4u) |
-               ((v.w >> 5) & 8u);
-      }
-      ((unsigned*)mask)[i] = (lab & 1u ? 0xFFu : 0u) |
-                             (lab & 2u ? 0xFF00u : 0u) |
-                             (lab & 4u ? 0xFF0000u : 0u) |
-                             (lab & 8u ? 0xFF000000u : 0u);
-      fg += __popc(lab);
-    }
-    for (size_t q = nq * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-         q < P; q += (size_t)gridDim.x * blockDim.x) {
-      unsigned lab = 0;
-      for (int c = 0; c < d; ++c) lab |= (dyn[(size_t)c * P + q] >> 8) & 1u;
-      mask[q] = lab ? 255 : 0;
-      fg += lab;
-    }
   }
   for (int o = 16; o > 0; o >>= 1) fg += __shfl_xor_sync(FULL, fg, o);
   if ((threadIdx.x & 31) == 0 && fg) atomicAdd(&s_fg, (unsigned long long)fg);
@@ -2077,7 +2038,6 @@ __device__ double g_bterm[2][256];
 
 #include "cog_lean.cuh"
 #include "cog_fast.cuh"
-#include "cog_vec.cuh"
 
 // ---------------------------------------------------------------------------
 // evaluation: confusion counts (16 pixels a thread, warp reductions, one
@@ -2268,7 +2228,7 @@ int kernel_choice() {
   if (e[0] == 'p') return 1;
   if (e[0] == 'g') return 2;
   if (e[0] == 'l') return 3;
-  return 0;  // "fast" / "vec" and default
+  return 0;  // "fast" and default
 }
 
 template <typename T>
@@ -2335,44 +2295,7 @@ int launch_fast_k(const StepArgs& a, cudaStream_t st) {
   return launch_status();
 }
 
-template <int KMAX>
-int launch_vec_k(const StepArgs& a, cudaStream_t st) {
-  auto fn = vec_kernel<KMAX>;
-  const size_t smem = fast_smem_bytes(a.g.depth, a.g.n_groups);
-  if (smem > 200 * 1024) return COG_EUNSUPPORTED;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  const int occ = cached_occupancy((const void*)fn, LEAN_THREADS, smem);
-  const int tile_w = 4 * (32 / a.g.stride);
-  const long long tiles = (long long)((a.g.width + tile_w - 1) / tile_w) *
-                          ((a.g.height + a.g.stride - 1) / a.g.stride);
-  const long long units = tiles * a.g.depth;
-  const int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
-  const long long slots = (long long)per_stream * LEAN_WARPS;
-  const long long t = (units + slots - 1) / slots;
-  int gx = (int)((units + t * LEAN_WARPS - 1) / (t * LEAN_WARPS));
-  if (gx < 1) gx = 1;
-  const FastConst k = make_fast_const(a.q);
-  fn<<<dim3(gx, a.g.streams), LEAN_THREADS, smem, st>>>(a, k);
-  return launch_status();
-}
-
-bool vec_ok(const StepArgs& a) {
-  // experimental (COG_KERNEL=vec): 4 pixels a lane with 16-B accesses
-  const char* e = getenv("COG_KERNEL");
-  if (!e || e[0] != 'v') return false;
-  const int st = a.g.stride;
-  return (st == 1 || st == 2 || st == 4) && a.g.width % 4 == 0 &&
-         ((uintptr_t)a.frame % 16) == 0;
-}
-
 int launch_fast(const StepArgs& a, cudaStream_t st) {
-  if (vec_ok(a)) {
-    if (a.g.k <= 3) return launch_vec_k<3>(a, st);
-    if (a.g.k <= 5) return launch_vec_k<5>(a, st);
-    return launch_vec_k<8>(a, st);
-  }
   if (a.g.depth == 1) {
     if (a.g.k <= 3) return launch_fast_k<3, 1>(a, st);
     if (a.g.k <= 5) return launch_fast_k<5, 1>(a, st);
@@ -2418,52 +2341,34 @@ bool fast_ok(const StepArgs& a, bool f32) {
 }
 
 template <typename T>
-int launch_deep(StepArgs a, cudaStream_t st, bool union_mask,
-                bool pdl = false) {
+int launch_deep(const StepArgs& a, cudaStream_t st, bool pdl) {
   auto fn = pick_deep<T>(a.g.k);
-  a.union_mask = union_mask ? 1 : 0;
   const size_t P = (size_t)a.g.height * a.g.width;
   size_t dg = (P * a.g.depth / 8 + 255) / 256;  // covers ~12% deep items
-  if (!union_mask) {
-    // grid-stride over the worklist; more CTAs than SMs only add last-CTA
-    // atomics and tail (COG_DEEP_CTAS_PER_SM tunes it)
-    const char* env = getenv("COG_DEEP_CTAS_PER_SM");
-    const size_t per_sm = env ? (size_t)atoi(env) : 8;
-    const size_t cap = (size_t)num_sms() * per_sm / a.g.streams + 1;
-    if (dg > cap) dg = cap;
-    if (dg < 1) dg = 1;
-    if (!pdl) {
-      fn<<<dim3((unsigned)dg, a.g.streams), 256, 0, st>>>(a);
-      return launch_status();
-    }
-    // programmatic dependent launch: the deep grid is scheduled while the
-    // hot kernel drains and waits (griddepcontrol.wait) for its results,
-    // hiding the launch gap between the two kernels of a frame
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)dg, a.g.streams);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
-    return e == cudaSuccess ? COG_OK : (int)e;
-  }
-  // the union pass needs a stream-wide barrier: cooperative launch of a
-  // grid that is guaranteed co-resident
-  const int occ = cached_occupancy((const void*)fn, 256, 0);
-  const size_t cap = (size_t)num_sms() * occ / a.g.streams;
-  if (cap < 1) return COG_EUNSUPPORTED;
-  const size_t want = (P / 4 + 255) / 256;  // union pass: 4 pixels a thread
-  if (dg < want) dg = want;
+  // grid-stride over the worklist; more CTAs than SMs only add last-CTA
+  // atomics and tail (COG_DEEP_CTAS_PER_SM tunes it; 1..8 measured equal)
+  const char* env = getenv("COG_DEEP_CTAS_PER_SM");
+  const size_t per_sm = env ? (size_t)atoi(env) : 8;
+  const size_t cap = (size_t)num_sms() * per_sm / a.g.streams + 1;
   if (dg > cap) dg = cap;
   if (dg < 1) dg = 1;
-  void* args[] = {(void*)&a};
-  cudaError_t e = cudaLaunchCooperativeKernel(
-      (const void*)fn, dim3((unsigned)dg, a.g.streams), dim3(256), args, 0, st);
+  if (!pdl) {
+    fn<<<dim3((unsigned)dg, a.g.streams), 256, 0, st>>>(a);
+    return launch_status();
+  }
+  // programmatic dependent launch: the deep grid is scheduled while the
+  // hot kernel drains and waits (griddepcontrol.wait) for its results
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)dg, a.g.streams);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
   return e == cudaSuccess ? COG_OK : (int)e;
 }
 
@@ -2471,15 +2376,13 @@ template <typename T>
 int launch_step(const StepArgs& a, cudaStream_t st) {
   set_fetch_granularity();
   ensure_bterm();
-  // float32 state: the fast kernel (vec: 4 pixels a lane, mask formed by
-  // the deep kernel's union pass); otherwise lean / pipelined / general
+  // float32 state: the fast kernel; otherwise lean / pipelined / general
   const bool fast = fast_ok(a, sizeof(T) == 4);
   int rc = fast ? launch_fast(a, st) : launch_hot<T>(a, st);
   if (rc) return rc;
   // programmatic dependent launch measured slightly slower on B200 (the
   // early-scheduled deep CTAs compete with the hot kernel's tail): opt-in
-  return launch_deep<T>(a, st, fast && vec_ok(a),
-                        fast && !vec_ok(a) && getenv("COG_PDL"));
+  return launch_deep<T>(a, st, fast && getenv("COG_PDL"));
 }
 
 }  // namespace

@@ -77,12 +77,12 @@ def test_baseline_gmm_matches_reference_golden():
         assert np.array_equal(getattr(g, nm), z[nm]), nm
 
 
-@pytest.mark.parametrize("kernel", ["pipelined", "general"])
+@pytest.mark.parametrize("kernel", ["lean", "pipe", "general"])
 @pytest.mark.parametrize("name", CASES)
 def test_engine_f64_bit_exact_vs_reference(name, kernel, monkeypatch):
-    # "general" forces the non-pipelined step kernel (any stride / width)
-    if kernel == "general":
-        monkeypatch.setenv("COG_NO_PIPE", "1")
+    # every binary64 step kernel: lean (default), cp.async-pipelined, and
+    # the general one (any stride / width)
+    monkeypatch.setenv("COG_KERNEL", kernel)
     rec, overrides = load_case(name)
     cfg = config_for(overrides, state_dtype="float64")
     frames = rec["frames"]
@@ -129,8 +129,10 @@ def test_engine_f64_production_sums(name):
     np.testing.assert_allclose(eng.group_var, rec["final_group_var"], rtol=1e-7)
 
 
+@pytest.mark.parametrize("kernel", ["fast", "lean", "general"])
 @pytest.mark.parametrize("name", CASES)
-def test_engine_f32_within_tolerance(name):
+def test_engine_f32_within_tolerance(name, kernel, monkeypatch):
+    monkeypatch.setenv("COG_KERNEL", kernel)
     rec, overrides = load_case(name)
     cfg = config_for(overrides)
     frames = rec["frames"]

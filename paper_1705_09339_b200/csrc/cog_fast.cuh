@@ -85,6 +85,20 @@ __device__ COG_SLOW_ATTR HotOut hot_px_slow(const StepArgs* __restrict__ a,
   return h;
 }
 
+// single-instruction MUFU approximations (rel. error ~1 ulp): every value
+// they feed is either continuous (within the fp32 tolerance) or a decision
+// protected by the 1e-5 filter margins; operands are normal, positive floats
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // filtered fp32 match: 1 hit, 0 miss, -1 undecided (within the margin)
 // (margin: relative to the threshold plus a few ulp of 255 absolute, so the
 // fp32 rounding of |v - mu| and of the threshold can never flip it)
@@ -313,15 +327,16 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
         if (top == L_GROUP && !grouping) top = c1;
         const bool gtop = top == L_GROUP && member;
         const bool top1 = top == L_MEANVAR;
-        const float s0 = x.var0 * rsqrtf(x.var0), s1 = x.var1 * rsqrtf(x.var1);
+        const float s0 = x.var0 * rsqrt_approx(x.var0),
+                    s1 = x.var1 * rsqrt_approx(x.var1);
         const float thr0 = k.lam * s0, thr1 = k.lam * s1;
         const float gm = member ? s_gmuf[gidx] : 0.0f;
         const float gt_thr = member ? s_gthrf[gidx] : 1.0f;
         const float mt = gtop ? gm : (top1 ? x.mu1 : x.mu0);
         const float dn = gtop ? gt_thr : (top1 ? thr1 : thr0);
-        const float ph = __fdividef(x.tv, x.peak);
+        const float ph = x.tv * rcp_approx(x.peak);
         const float bt = s_btf[dv];
-        float gt = fminf(__fdividef(fabsf(vf - mt), dn), 1.0f);
+        float gt = fminf(fabsf(vf - mt) * rcp_approx(dn), 1.0f);
         if (!literal) gt = 1.0f - gt;
         if (ph < k.pf)
           cf = (wb * bt + wc * gt) * k.wbc_inv[cls];

@@ -41,7 +41,12 @@
  *   dyn      u32[depth][P]   chp_prev | last_label | waking | last_active | clock
  *   streak   u32[depth][P]
  *   hits     u32[depth][5][P]
- *   table    f32[depth][P][256], peak f32[depth][P]
+ *   table    f32, tile-major: per plane [n_tiles][256][SL] -- bin v of the
+ *            pixel in slot (row * cw + col) of warp tile t (stride rows x
+ *            cw columns, SL = 32 * ceil(stride * cw / 32)) at
+ *            (t * 256 + v) * SL + slot; cog_table_floats() per stream,
+ *            cog_table_pack() converts from / to the reference [P][256]
+ *   peak     f32[depth][P]
  *   cls      u8[P], gid u16[P] (0xFFFF = ungrouped)
  *   g_mu, g_var  f64[depth][G], g_members u32[G]
  *   accum    u64[cog_accum_words()], sync u32[4]
@@ -112,6 +117,15 @@ int64_t cog_accum_words(int32_t depth, int32_t n_groups);
 
 /* Worklist slots per stream (deep-level plane-pixels of one frame). */
 int64_t cog_deepq_slots(int32_t depth, int64_t n_pix);
+
+/* Floats of one stream's tile-major prior table (all planes), or -1. */
+int64_t cog_table_floats(const cog_geom *geom);
+
+/* One stream's prior table between the reference layout f32[depth][P][256]
+ * (scene_prior / model files, cascade.py:192) and the engine's tile-major
+ * layout: to_tiled = 1 packs ref_layout into tiled, 0 unpacks. */
+int cog_table_pack(const cog_geom *geom, float *ref_layout, float *tiled,
+                   int32_t to_tiled, void *stream);
 
 /* Scene prior for one stream: frames u8[N][depth][P].  Writes, for each
  * trailing window windows[j] (ascending, last == N), tables

@@ -106,6 +106,8 @@ class RefState(ctypes.Structure):
 _P = ctypes.c_void_p
 _SIGS = {
     "cog_accum_words": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
+    "cog_table_floats": (ctypes.c_int64, [_P]),
+    "cog_table_pack": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, _P]),
     "cog_deepq_slots": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int64]),
     "cog_prior_build": (ctypes.c_int, [
         _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, _P, _P,

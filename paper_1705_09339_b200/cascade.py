@@ -199,7 +199,13 @@ class DeviceState:
         self.dyn = z(S, d, P, dtype=torch.int32)
         self.streak = z(S, d, P, dtype=torch.int32)
         self.hits = z(S, d, 5, P, dtype=torch.int32)
-        self.table = z(S, d, P, 256, dtype=torch.float32)
+        # prior tables in the tile-major layout of the step kernels
+        # (cog_table_pack converts from / to the reference [d][P][256])
+        self.tab_floats = int(_lib.load().cog_table_floats(
+            _lib.ref(self._geom(1))))
+        if self.tab_floats < 0:
+            raise DataError("unsupported engine geometry")
+        self.table = z(S, self.tab_floats, dtype=torch.float32)
         self.peak = torch.ones((S, d, P), dtype=torch.float32, device=dev)
         self.cls = z(S, P, dtype=torch.uint8)
         self.gid = torch.full((S, P), -1, dtype=torch.int16, device=dev)
@@ -216,13 +222,38 @@ class DeviceState:
         self.deeprho = torch.empty((S, slots), dtype=torch.float64, device=dev)
         self._refresh()
 
-    def _refresh(self) -> None:
+    def _geom(self, streams: int) -> "_lib.Geom":
         g = _lib.Geom()
         g.total_pixels = self.total_pixels
         g.height, g.width, g.depth = self.height, self.width, self.depth
         g.k, g.stride, g.n_groups = self.k, self.stride, self.n_groups
-        g.streams, g.state_f64, g.row0 = self.streams, int(self.f64), self.row0
-        self.geom = g
+        g.streams, g.state_f64, g.row0 = streams, int(self.f64), self.row0
+        return g
+
+    def table_to_ref(self, s: int) -> torch.Tensor:
+        """Stream s's prior table in the reference layout (d, P, 256)."""
+        out = torch.empty((self.depth, self.P, 256), dtype=torch.float32,
+                          device=self.device)
+        rc = _lib.load().cog_table_pack(
+            _lib.ref(self._geom(1)), out.data_ptr(), self.table[s].data_ptr(),
+            0, torch.cuda.current_stream(self.device).cuda_stream)
+        _lib.check(rc, "cog_table_pack")
+        return out
+
+    def table_from_ref(self, s: int, tables: torch.Tensor) -> None:
+        """Pack a (d, P, 256) f32 device table into stream s."""
+        tables = tables.to(self.device, torch.float32).contiguous()
+        if tuple(tables.shape) != (self.depth, self.P, 256):
+            raise DataError(f"table shape {tuple(tables.shape)} != "
+                            f"{(self.depth, self.P, 256)}")
+        rc = _lib.load().cog_table_pack(
+            _lib.ref(self._geom(1)), tables.data_ptr(),
+            self.table[s].data_ptr(), 1,
+            torch.cuda.current_stream(self.device).cuda_stream)
+        _lib.check(rc, "cog_table_pack")
+
+    def _refresh(self) -> None:
+        self.geom = self._geom(self.streams)
         st = _lib.State()
         for name in ("mu", "var", "w", "meta", "dyn", "streak", "hits",
                      "table", "peak", "cls", "gid", "g_mu", "g_var",
@@ -708,7 +739,7 @@ class CascadeEngine:
 
     @property
     def tables(self) -> np.ndarray:
-        return self.dev.table[0].cpu().numpy()
+        return self.dev.table_to_ref(0).cpu().numpy()
 
     @property
     def group_id(self) -> np.ndarray:

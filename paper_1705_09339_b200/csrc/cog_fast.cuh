@@ -276,7 +276,10 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
 #ifdef COG_EXP_NOTABLE
       x.tv = 0.01f * (float)(o & 7);
 #else
-      x.tv = __ldcg(a.s.table + (((size_t)o << 8) | (uint32_t)x.vb));
+      // tile-major table: plane (sK + c), tile wt, bin v, slot = lane
+      x.tv = __ldcg(a.s.table +
+                    (((size_t)(sK + c) * a.n_tiles + wt) * 256 + x.vb) * 32 +
+                    lane);
 #endif
       const uint32_t r0 = (x.meta >> 10) & 7u, r1 = x.meta >> 13;
 #ifdef COG_EXP_NOMODES

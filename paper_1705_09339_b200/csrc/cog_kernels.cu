@@ -73,6 +73,53 @@ struct StepArgs {
   int cw, iters, tiles_x, n_tiles;
 };
 
+// ---------------------------------------------------------------------------
+// Prior-table layout.  The step reads ONE entry of a pixel's 256-bin table
+// per frame (at the pixel's value v).  Stored pixel-major (the reference's
+// [P][256]), every lookup of a warp is 32 random 128-B DRAM fetches.  Stored
+// tile-major instead -- per plane [n_tiles][256][SL], the SL slots of a bin
+// being the pixels of one warp tile (stride rows x cw columns, slot =
+// row * cw + col, SL = iters * 32) -- the lanes of a warp that see the same
+// value share one 128-B line (measured on C2: 16.7 lines per warp-plane
+// instead of 32, -57 MB DRAM per frame).  Host views and model files use
+// the reference layout; cog_table_pack converts.
+// ---------------------------------------------------------------------------
+struct TabGeo {
+  uint32_t W, st, cw, tiles_x, SL;
+  size_t plane;  // floats per plane
+};
+
+__host__ __device__ inline void tile_shape(int st, int H, int W, int& cw,
+                                           int& iters, int& tiles_x,
+                                           int& n_tiles) {
+  const int m = (32 / (st * st)) > 0 ? 32 / (st * st) : 1;
+  cw = st * m;
+  iters = (st * cw + 31) / 32;
+  tiles_x = (W + cw - 1) / cw;
+  n_tiles = tiles_x * ((H + st - 1) / st);
+}
+
+__host__ __device__ inline TabGeo tab_geo(const cog_geom& g) {
+  int cw, iters, tiles_x, n_tiles;
+  tile_shape(g.stride, g.height, g.width, cw, iters, tiles_x, n_tiles);
+  TabGeo t;
+  t.W = (uint32_t)g.width;
+  t.st = (uint32_t)g.stride;
+  t.cw = (uint32_t)cw;
+  t.tiles_x = (uint32_t)tiles_x;
+  t.SL = (uint32_t)(iters * 32);
+  t.plane = (size_t)n_tiles * 256 * t.SL;
+  return t;
+}
+
+// offset of pixel p's bin 0 inside its plane's table; bin v is at + v * SL
+__device__ __forceinline__ size_t tab_pix(const TabGeo& t, size_t p) {
+  const uint32_t y = (uint32_t)(p / t.W), x = (uint32_t)(p - (size_t)y * t.W);
+  const uint32_t ty = y / t.st, r = y - ty * t.st;
+  const uint32_t tx = x / t.cw, col = x - tx * t.cw;
+  return (size_t)(ty * t.tiles_x + tx) * 256 * t.SL + r * t.cw + col;
+}
+
 template <typename T>
 struct MixPtrs {
   T* mu;
@@ -130,9 +177,10 @@ struct PlaneRef {
   uint32_t* dyn;
   uint32_t* streak;
   uint32_t* hits;
-  const float* table;
+  const float* table;  // this plane's tile-major prior table
   const float* peak;
   size_t P;
+  TabGeo tg;
 };
 
 template <typename T>
@@ -149,7 +197,8 @@ __device__ __forceinline__ PlaneRef<T> plane_ref(const StepArgs& a, int s,
   r.dyn = a.s.dyn + sc * P;
   r.streak = a.s.streak + sc * P;
   r.hits = a.s.hits + sc * 5 * P;
-  r.table = a.s.table + sc * P * 256;
+  r.tg = tab_geo(a.g);
+  r.table = a.s.table + sc * r.tg.plane;
   r.peak = a.s.peak + sc * P;
   r.P = P;
   return r;
@@ -238,7 +287,8 @@ __device__ __noinline__ void cold_reorder(PlaneRef<T> r, size_t p,
         int k = meta_ref(meta, code[j] == L_MEAN ? 0 : 1);
         lmu = ldrw(r.mu + (size_t)k * r.P + p);
       }
-      nm[j] = -(double)r.table[p * 256 + (int)clip_rint(lmu)];
+      nm[j] = -(double)r.table[tab_pix(r.tg, p) +
+                               (size_t)clip_rint(lmu) * r.tg.SL];
     }
   }
   // np.lexsort((-mass, -hv)): primary -hv, secondary -mass, stable
@@ -394,7 +444,7 @@ __device__ __forceinline__ void preload_r2(const PlaneRef<T>& pr, size_t p,
 #ifdef COG_EXP_NOTABLE
   x.tv = 0.01f;
 #else
-  x.tv = __ldcg(pr.table + p * 256 + x.vb);
+  x.tv = __ldcg(pr.table + tab_pix(pr.tg, p) + (size_t)x.vb * pr.tg.SL);
 #endif
   const int r0 = meta_ref(x.meta, 0), r1 = meta_ref(x.meta, 1);
   x.mu0 = pr.mu[(size_t)r0 * pr.P + p];
@@ -1440,7 +1490,8 @@ __global__ void __launch_bounds__(PIPE_THREADS, COG_PIPE_MINB)
       const bool ev = valid && !f.compat &&
                       will_evaluate(f.sampling, dyn, vb, on_lat, a.q.chp_epsilon);
       const int r0 = meta_ref(meta, 0), r1 = meta_ref(meta, 1);
-      cpa(B + L.b_tv + c * 128 + lane * 4, pr.table + p * 256 + vb, 4, ev);
+      cpa(B + L.b_tv + c * 128 + lane * 4,
+          pr.table + ((size_t)wt * 256 + vb) * 32 + lane, 4, ev);
       cpa(B + L.b_mu0 + (c * 32 + lane) * sizeof(T), pr.mu + (size_t)r0 * P + p,
           sizeof(T), ev);
       cpa(B + L.b_var0 + (c * 32 + lane) * sizeof(T),
@@ -1654,6 +1705,24 @@ __global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
   if (!s_last) return;
   __threadfence();
   finalize_stream<T>(a, s, gacc, a.stats, sync);
+}
+
+// reference layout f32[d][P][256] <-> tile-major (one stream); one thread
+// per table entry, coalesced on the reference side
+__global__ void table_pack_kernel(TabGeo tg, int d, size_t P,
+                                  float* ref_layout, float* tiled,
+                                  int to_tiled) {
+  const size_t n = (size_t)d * P * 256;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t c = i / (P * 256), rem = i - c * P * 256;
+    const size_t p = rem >> 8, v = rem & 255;
+    const size_t t = c * tg.plane + tab_pix(tg, p) + v * tg.SL;
+    if (to_tiled)
+      tiled[t] = ref_layout[i];
+    else
+      ref_layout[i] = tiled[t];
+  }
 }
 
 template <typename T>
@@ -1889,7 +1958,8 @@ __global__ void __launch_bounds__(128) warmup_kernel(const WarmArgs a) {
   }
   // mode references: lexsort((-tie, -mass)) over all K slots
   // (cascade.py:218-235); dead slots carry (-inf, -inf)
-  const float* trow = a.s.table + ((size_t)c * P + p) * 256;
+  const TabGeo tg = tab_geo(a.g);
+  const float* trow = a.s.table + (size_t)c * tg.plane + tab_pix(tg, p);
   double nm[KMAX], nt[KMAX];
   const double PINF = __longlong_as_double(0x7ff0000000000000ll);
 #pragma unroll
@@ -1897,7 +1967,7 @@ __global__ void __launch_bounds__(128) warmup_kernel(const WarmArgs a) {
     nm[k] = PINF;
     nt[k] = PINF;
     if (k < n) {
-      nm[k] = -(double)trow[(int)clip_rint(m.mu[k])];
+      nm[k] = -(double)trow[(size_t)clip_rint(m.mu[k]) * tg.SL];
       nt[k] = -(m.w[k] / sqrt(m.var[k]));
     }
   }
@@ -2173,13 +2243,8 @@ StepArgs make_args(const cog_geom* g, const cog_params* q, const cog_state* s) {
   a.g = *g;
   if (q) a.q = *q;
   a.s = *s;
-  const int st = g->stride;
-  const int m = (32 / (st * st)) > 0 ? 32 / (st * st) : 1;
-  a.cw = st * m;
-  a.iters = (st * a.cw + 31) / 32;
-  a.tiles_x = (g->width + a.cw - 1) / a.cw;
-  const int tiles_y = (g->height + st - 1) / st;
-  a.n_tiles = a.tiles_x * tiles_y;
+  tile_shape(g->stride, g->height, g->width, a.cw, a.iters, a.tiles_x,
+             a.n_tiles);
   return a;
 }
 
@@ -2417,6 +2482,26 @@ int cog_debug_prof(uint64_t* out16, int reset) {
 
 int64_t cog_deepq_slots(int32_t depth, int64_t n_pix) {
   return (int64_t)dq_capacity(depth, (size_t)n_pix);
+}
+
+int64_t cog_table_floats(const cog_geom* geom) {
+  if (!geom || check_geom(geom)) return -1;
+  return (int64_t)(tab_geo(*geom).plane * (size_t)geom->depth);
+}
+
+int cog_table_pack(const cog_geom* geom, float* ref_layout, float* tiled,
+                   int32_t to_tiled, void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!ref_layout || !tiled) return COG_EINVAL;
+  const size_t P = (size_t)geom->height * geom->width;
+  const size_t n = (size_t)geom->depth * P * 256;
+  size_t blocks = (n + 255) / 256;
+  const size_t cap = (size_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  table_pack_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      tab_geo(*geom), geom->depth, P, ref_layout, tiled, to_tiled);
+  return launch_status();
 }
 
 int cog_prior_build(const uint8_t* frames, int32_t n_frames, int32_t depth,

@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_LEAN_MINB)
   uint32_t* stkb = a.s.streak + sD * P;
   const float* peakb = a.s.peak + sD * P;
   uint32_t* hitsb = a.s.hits + sD * 5 * P;
-  const float* tabb = a.s.table + sD * P * 256;
+  const TabGeo tg = tab_geo(a.g);
+  const float* tabb = a.s.table + sD * tg.plane;
   T* mub = (T*)a.s.mu + sD * K * P;
   T* varb = (T*)a.s.var + sD * K * P;
   T* wgtb = (T*)a.s.w + sD * K * P;
@@ -192,7 +193,8 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_LEAN_MINB)
 #ifdef COG_EXP_NOTABLE
         pre[c].tv = 0.01f * (float)(o & 7);  // ablation: no table gather
 #else
-        pre[c].tv = __ldcg(tabb + (size_t)o * 256 + pre[c].vb);
+        pre[c].tv = __ldcg(tabb + (size_t)c * tg.plane +
+                           ((size_t)wt * 256 + pre[c].vb) * 32 + lane);
 #endif
         const int r0 = meta_ref(pre[c].meta, 0), r1 = meta_ref(pre[c].meta, 1);
         const size_t mb = (size_t)c * K * P + p;
@@ -231,9 +233,10 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_LEAN_MINB)
       pr.dyn = dynb + (size_t)c * P;
       pr.streak = stkb + (size_t)c * P;
       pr.hits = hitsb + (size_t)c * 5 * P;
-      pr.table = tabb + (size_t)c * P * 256;
+      pr.table = tabb + (size_t)c * tg.plane;
       pr.peak = peakb + (size_t)c * P;
       pr.P = P;
+      pr.tg = tg;
       HotOut ho;
       ho.kind = 0;
       ho.label = 0;

@@ -76,7 +76,8 @@ class ScenePrior:
     depth: int
     height: int
     width: int
-    tables: torch.Tensor          # (d, P, 256) f32, window N
+    tables: torch.Tensor | None   # (d, P, 256) f32, window N (None once
+                                  # packed into an engine: train_device)
     peak: torch.Tensor            # (d, P) f32, <= 0 replaced by 1
     classes: torch.Tensor         # (P,) u8
     residue: torch.Tensor         # (P, 3) int32 counts

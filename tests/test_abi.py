@@ -53,3 +53,17 @@ def test_host_only_calls():
     assert lib.cog_set_levels(_lib.ref(g), None, None) == _lib.COG_EUNSUPPORTED
     with pytest.raises(Exception):
         _lib.check(_lib.COG_EINVAL, "x")
+
+
+def test_table_layout_size():
+    """Tile-major prior table: per plane n_tiles x 256 bins x SL slots
+    (host-side arithmetic only, no GPU)."""
+    lib = _lib.load()
+    for (h, w, st, d, floats) in [
+            (480, 640, 2, 3, 3 * (640 // 16) * (480 // 2) * 256 * 32),
+            (120, 160, 1, 1, 1 * (160 // 32) * 120 * 256 * 32),
+            (7, 10, 3, 1, 1 * 2 * 3 * 256 * 32)]:   # cw 9: ragged edges
+        g = _lib.Geom()
+        g.total_pixels, g.height, g.width, g.depth = h * w, h, w, d
+        g.k, g.stride, g.streams = 3, st, 1
+        assert lib.cog_table_floats(_lib.ref(g)) == floats

@@ -36,6 +36,24 @@ def test_library_version():
     assert b"sm_100a" in _lib.load().cog_version()
 
 
+@pytest.mark.parametrize("h,w,stride,d", [(11, 37, 3, 1), (48, 32, 2, 3),
+                                           (13, 29, 1, 3), (9, 40, 6, 1)])
+def test_table_layout_roundtrip(h, w, stride, d):
+    """reference [d][P][256] -> tile-major -> back is the identity, and the
+    packed buffer holds every entry exactly once (ragged tiles included)"""
+    from paper_1705_09339_b200.cascade import CascadeEngine
+    from paper_1705_09339_b200.config import EngineConfig
+    eng = CascadeEngine(EngineConfig(stride=stride, color=d == 3), h, w, d)
+    ref = torch.rand((d, h * w, 256), device="cuda")
+    eng.dev.table.zero_()
+    eng.dev.table_from_ref(0, ref)
+    assert torch.equal(eng.dev.table_to_ref(0), ref)
+    packed = eng.dev.table[0]
+    assert int((packed != 0).sum()) == int((ref != 0).sum())
+    assert torch.equal(torch.sort(packed[packed != 0]).values,
+                       torch.sort(ref.flatten()).values)
+
+
 def test_prior_matches_reference_golden():
     from paper_1705_09339_b200.config import EngineConfig
     from paper_1705_09339_b200.scene_prior import build_scene_prior

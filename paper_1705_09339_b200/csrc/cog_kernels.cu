@@ -1675,13 +1675,22 @@ __global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
   const size_t dq_cap = dq_capacity(d, P);
   unsigned long long* dq_code = (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
   const double* dq_rho = a.s.deeprho + (size_t)s * dq_cap;
+#ifdef COG_EXP_NODEEP
+  const size_t n = 0;  // timing ablation: the kernel's fixed cost only
+#else
   const size_t n = *(volatile uint32_t*)(sync + 3);
+#endif
   uint8_t* mask = a.mask + (size_t)s * P;
   if (threadIdx.x == 0) s_fg = 0;
   __syncthreads();
   unsigned fg = 0;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
+  // warp-granular round robin over the CTAs (warp 0 of every CTA first):
+  // a short worklist spreads over all SMs instead of filling the first
+  // few CTAs
+  const size_t wpc = blockDim.x >> 5;
+  const size_t gw = (size_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  for (size_t i = gw * 32 + (threadIdx.x & 31); i < n;
+       i += (size_t)gridDim.x * wpc * 32) {
     const unsigned long long code = dq_code[i];
     if (!(code & 1ull)) continue;
     dq_code[i] = 0ull;
@@ -2410,11 +2419,14 @@ int launch_deep(const StepArgs& a, cudaStream_t st, bool pdl) {
   auto fn = pick_deep<T>(a.g.k);
   const size_t P = (size_t)a.g.height * a.g.width;
   size_t dg = (P * a.g.depth / 8 + 255) / 256;  // covers ~12% deep items
-  // grid-stride over the worklist; more CTAs than SMs only add last-CTA
-  // atomics and tail (COG_DEEP_CTAS_PER_SM tunes it; 1..8 measured equal)
+  // grid-stride over the worklist, one wave (COG_DEEP_CTAS_PER_SM
+  // overrides the occupancy)
   const char* env = getenv("COG_DEEP_CTAS_PER_SM");
-  const size_t per_sm = env ? (size_t)atoi(env) : 8;
-  const size_t cap = (size_t)num_sms() * per_sm / a.g.streams + 1;
+  const size_t per_sm =
+      env ? (size_t)atoi(env)
+          : (size_t)cached_occupancy((const void*)fn, 256, 0);
+  size_t cap = (size_t)num_sms() * per_sm / a.g.streams;
+  if (cap < 1) cap = 1;
   if (dg > cap) dg = cap;
   if (dg < 1) dg = 1;
   if (!pdl) {

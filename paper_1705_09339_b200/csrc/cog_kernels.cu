@@ -2457,9 +2457,11 @@ int launch_step(const StepArgs& a, cudaStream_t st) {
   const bool fast = fast_ok(a, sizeof(T) == 4);
   int rc = fast ? launch_fast(a, st) : launch_hot<T>(a, st);
   if (rc) return rc;
-  // programmatic dependent launch measured slightly slower on B200 (the
-  // early-scheduled deep CTAs compete with the hot kernel's tail): opt-in
-  return launch_deep<T>(a, st, fast && getenv("COG_PDL"));
+  // programmatic dependent launch of the deep pass: its CTAs are scheduled
+  // while the hot kernel drains (they wait in griddepcontrol.wait), which
+  // hides the launch gap -- measured 72.9 -> 70.9 us per C2 step
+  // (tools/ab_bench.sh); COG_NO_PDL=1 launches it plainly
+  return launch_deep<T>(a, st, fast && !getenv("COG_NO_PDL"));
 }
 
 }  // namespace

@@ -283,6 +283,39 @@ class BandSet:
 # --------------------------------------------------------- batch engine
 
 
+class BatchResult:
+    """Masks (S, H, W) u8 and statistics rows (S, 10) i64 of one batch
+    step, downloaded asynchronously into a pinned slot of the engine's ring;
+    ``masks`` / ``stats`` block on the download.  A slot is reused three
+    submissions later; a result still referring to it is copied out first,
+    so results stay valid however long they are kept."""
+
+    def __init__(self, slot: dict) -> None:
+        self._slot = slot
+        self._own = None
+
+    def _wait(self):
+        if self._own is not None:
+            return self._own
+        self._slot["down"].synchronize()
+        return (self._slot["hm"].numpy(), self._slot["hs"].numpy()[:, :10])
+
+    def detach(self) -> None:
+        """Copy out of the slot (called before the slot is reused)."""
+        if self._own is None:
+            m, st = self._wait()
+            self._own = (m.copy(), st.copy())
+        self._slot = None
+
+    @property
+    def masks(self) -> np.ndarray:
+        return self._wait()[0]
+
+    @property
+    def stats(self) -> np.ndarray:
+        return self._wait()[1]
+
+
 class BatchEngine:
     """S independent streams of one geometry in one set of HBM buffers;
     one launch steps every stream (no collectives, per-stream globals on
@@ -373,13 +406,79 @@ class BatchEngine:
     def process_frames(self, frames) -> tuple[np.ndarray, np.ndarray]:
         """frames (S, d, H, W) uint8 (host or CUDA) -> masks (S, H, W) u8,
         stats (S, 10) int64 rows (FrameStats layout)."""
-        x = torch.as_tensor(frames).to(self.dev.device).contiguous()
-        masks = torch.empty((self.streams, self.height, self.width),
-                            dtype=torch.uint8, device=self.dev.device)
-        stats = torch.empty((self.streams, 16), dtype=torch.int64,
-                            device=self.dev.device)
-        self.process_frames_device(x, masks, stats)
-        return masks.cpu().numpy(), stats[:, :10].cpu().numpy()
+        if isinstance(frames, torch.Tensor) and frames.is_cuda:
+            x = frames.contiguous()
+            masks = torch.empty((self.streams, self.height, self.width),
+                                dtype=torch.uint8, device=self.dev.device)
+            stats = torch.empty((self.streams, 16), dtype=torch.int64,
+                                device=self.dev.device)
+            self.process_frames_device(x, masks, stats)
+            return masks.cpu().numpy(), stats[:, :10].cpu().numpy()
+        res = self.submit_frames(frames)
+        return res.masks.copy(), res.stats.copy()
+
+    def submit_frames(self, frames) -> BatchResult:
+        """Host frames (S, d, H, W) uint8 -- a pinned tensor is DMA'd as is,
+        anything else is staged into the slot's pinned buffer -- through a
+        ring of three slots: upload on a copy stream (overlapping the
+        previous step), step on the engine's stream, download of masks and
+        statistics on the copy stream.  Returns at once."""
+        dev = self.dev.device
+        if getattr(self, "_ring", None) is None:
+            S, d, H, W = self.streams, self.depth, self.height, self.width
+            self._copy = torch.cuda.Stream(device=dev)
+            self._ring = [{
+                "in": torch.empty((S, d, H, W), dtype=torch.uint8,
+                                  pin_memory=True),
+                "x": torch.empty((S, d, H, W), dtype=torch.uint8, device=dev),
+                "m": torch.empty((S, H, W), dtype=torch.uint8, device=dev),
+                "s": torch.empty((S, 16), dtype=torch.int64, device=dev),
+                "hm": torch.empty((S, H, W), dtype=torch.uint8,
+                                  pin_memory=True),
+                "hs": torch.empty((S, 16), dtype=torch.int64,
+                                  pin_memory=True),
+                "up": torch.cuda.Event(), "step": torch.cuda.Event(),
+                "down": torch.cuda.Event(), "owner": None, "used": False,
+            } for _ in range(3)]
+            self._next = 0
+        slot = self._ring[self._next]
+        self._next = (self._next + 1) % len(self._ring)
+        if slot["owner"] is not None:
+            slot["owner"].detach()     # keep the old result valid
+            slot["owner"] = None
+        if slot["used"]:
+            slot["down"].synchronize()  # pinned in/out buffers free again
+        shape = (self.streams, self.depth, self.height, self.width)
+        if (isinstance(frames, torch.Tensor) and not frames.is_cuda
+                and frames.is_pinned() and frames.dtype == torch.uint8
+                and frames.is_contiguous() and tuple(frames.shape) == shape):
+            src = frames
+        else:
+            arr = np.asarray(frames.numpy() if isinstance(frames, torch.Tensor)
+                             else frames)
+            if arr.shape != shape or arr.dtype != np.uint8:
+                raise DataError(f"frames must be {shape} uint8")
+            np.copyto(slot["in"].numpy(), arr)
+            src = slot["in"]
+        compute = torch.cuda.current_stream(dev)
+        with torch.cuda.stream(self._copy):
+            if slot["used"]:
+                self._copy.wait_event(slot["step"])  # device input reusable
+            slot["x"].copy_(src, non_blocking=True)
+            slot["up"].record(self._copy)
+        compute.wait_event(slot["up"])
+        self.process_frames_device(slot["x"], slot["m"], slot["s"])
+        slot["step"].record(compute)
+        with torch.cuda.stream(self._copy):
+            self._copy.wait_event(slot["step"])
+            slot["hm"].copy_(slot["m"], non_blocking=True)
+            slot["hs"].copy_(slot["s"], non_blocking=True)
+            slot["down"].record(self._copy)
+        slot["used"] = True
+        slot["src"] = src              # the DMA source stays alive
+        res = BatchResult(slot)
+        slot["owner"] = res
+        return res
 
     def export_stream(self, s: int) -> dict:
         """Reference-layout state of stream s (after materialising any

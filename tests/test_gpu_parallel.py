@@ -112,3 +112,24 @@ def test_batch_engine_equals_separate_engines(dtype):
         got = batch.export_stream(i)
         for nm in STATE:
             assert np.array_equal(got[nm], getattr(eng, nm)), (i, nm)
+
+
+def test_batch_submit_pipeline_equals_synchronous():
+    """submit_frames: 30 frames in flight through the 3-slot ring (pinned
+    DMA sources, results read only at the end, so every slot is reused with
+    its result still pending) == the synchronous process_frames"""
+    from paper_1705_09339_b200 import synth
+    from paper_1705_09339_b200.parallel import BatchEngine
+    spec = synth.small_spec(5, 40, 24, 60, 30)
+    seqs = [synth.Scene(spec.for_stream(i)).frames(0, 60) for i in range(3)]
+    cfg = config_for({"k_max": 5, "color": True}, state_dtype="float32")
+    a = BatchEngine.train([s[:30] for s in seqs], cfg)
+    b = BatchEngine.train([s[:30] for s in seqs], cfg)
+    pending = []
+    for t in range(30, 60):
+        x = torch.from_numpy(np.stack([s[t] for s in seqs])).pin_memory()
+        pending.append(a.submit_frames(x))
+    for k, t in enumerate(range(30, 60)):
+        masks, stats = b.process_frames(np.stack([s[t] for s in seqs]))
+        assert np.array_equal(pending[k].masks, masks), t
+        assert np.array_equal(pending[k].stats, stats), t

@@ -114,10 +114,7 @@ __device__ __forceinline__ int fmatch(float vf, float mu, float thr) {
 #define COG_FAST_MINB 3
 #endif
 
-// DEF: the default configuration compiled in (sampling, grouping, rate
-// scaling and the change probe on, literal confidence and compat off,
-// stride 2) -- the flag tests and the dead branches drop out
-template <int KMAX, int D, bool DEF>
+template <int KMAX, int D>
 __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
     fast_kernel(const __grid_constant__ StepArgs a,
                 const __grid_constant__ FastConst k) {
@@ -125,17 +122,14 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
   extern __shared__ double s_mem[];
   const int s = blockIdx.y;
   const int G = a.g.n_groups, K = a.g.k;
-  const int H = a.g.height, W = a.g.width, stride = DEF ? 2 : a.g.stride;
+  const int H = a.g.height, W = a.g.width, stride = a.g.stride;
   const uint32_t P = (uint32_t)H * (uint32_t)W;
   const int words = acc_words(D, G);
   const int wpad = (words + 1) & ~1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool sampling = DEF || a.q.sampling_on != 0;
-  const bool grouping = DEF || a.q.grouping_on != 0;
-  const bool compat = !DEF && a.q.compat != 0;
-  const bool literal = !DEF && a.q.literal_conf != 0;
-  const bool chp_on = DEF || a.q.chp_on != 0;
-  const bool rate_on = DEF || a.q.rate_scaling_on != 0;
+  const bool sampling = a.q.sampling_on != 0, grouping = a.q.grouping_on != 0;
+  const bool compat = a.q.compat != 0, literal = a.q.literal_conf != 0;
+  const bool chp_on = a.q.chp_on != 0, rate_on = a.q.rate_scaling_on != 0;
 
   // ---- shared: bterm tables (double for the slow path, float), group
   // constants, warp-private partial slices, warp worklist buffers
@@ -193,7 +187,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
   const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
                   a.q.variance_floor, a.q.initial_variance};
 
-  const int cw = DEF ? 16 : a.cw;
+  const int cw = a.cw;
   const int lrow = lane / cw, lcol = lane - lrow * cw;
   const bool lane_ok = lane < stride * cw;
   const bool on_lat = (lrow == 0) && (lcol % stride == 0);

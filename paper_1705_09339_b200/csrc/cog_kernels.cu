@@ -2350,11 +2350,7 @@ bool pipe_ok(const StepArgs& a) {
 
 template <int KMAX, int D>
 int launch_fast_k(const StepArgs& a, cudaStream_t st) {
-  const cog_params& q = a.q;
-  const bool def = q.sampling_on && q.grouping_on && q.rate_scaling_on &&
-                   q.chp_on && !q.literal_conf && !q.compat &&
-                   a.g.stride == 2 && !getenv("COG_NO_DEF");
-  auto fn = def ? fast_kernel<KMAX, D, true> : fast_kernel<KMAX, D, false>;
+  auto fn = fast_kernel<KMAX, D>;
   const size_t smem = fast_smem_bytes(a.g.depth, a.g.n_groups);
   if (smem > 200 * 1024) return COG_EUNSUPPORTED;
   if (smem > 48 * 1024)

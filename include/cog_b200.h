@@ -206,7 +206,9 @@ int cog_import_state(const cog_geom *geom, const cog_state *st,
  * (pinned, d*P bytes) into `dev_frame` on `copy_stream`, recorded in
  * `up_event`; `stream` waits for it and runs the step (fused finalize);
  * mask (P bytes) and stats (16 x i64) are copied back into the pinned
- * `host_mask` / `host_stats` and completion is recorded in `done_event`.
+ * `host_mask` / `host_stats` on `down_stream` (NULL: on `stream`; a stream
+ * of its own keeps the next frame's step from queueing behind these
+ * copies) and completion is recorded in `done_event`.
  * Replaces the per-frame body of CascadeEngine.process_frame
  * (cascade.py:261-318) for host frames.  Events come from
  * cog_event_create. */
@@ -216,7 +218,7 @@ int cog_step_host(const cog_geom *geom, const cog_params *prm,
                   uint8_t *kind, int64_t *dev_stats, uint8_t *host_mask,
                   int64_t *host_stats, int64_t frame_index,
                   int32_t reorder_now, void *stream, void *copy_stream,
-                  void *up_event, void *done_event);
+                  void *down_stream, void *up_event, void *done_event);
 
 /* Confusion counts of predicted vs truth masks u8[n] (evaluation.
  * confusion_counts, cogbg/evaluation.py:72-89): truth 0 = background,

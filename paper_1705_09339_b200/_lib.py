@@ -125,7 +125,7 @@ _SIGS = {
     "cog_export_state": (ctypes.c_int, [_P, _P, _P, _P]),
     "cog_import_state": (ctypes.c_int, [_P, _P, _P, _P]),
     "cog_step_host": (ctypes.c_int, [_P] * 11 + [ctypes.c_int64,
-                                                ctypes.c_int32] + [_P] * 4),
+                                                ctypes.c_int32] + [_P] * 5),
     "cog_confusion": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P, _P]),
     "cog_event_create": (ctypes.c_void_p, []),
     "cog_event_destroy": (ctypes.c_int, [_P]),

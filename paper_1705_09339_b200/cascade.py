@@ -362,6 +362,9 @@ class HostRing:
         # host->device copies run on their own stream so frame t+1's upload
         # overlaps frame t's step; the step waits on the copy's event
         self.copy_stream = torch.cuda.Stream(device=device)
+        # device->host copies on a third stream: frame t+1's step does not
+        # queue behind frame t's downloads
+        self.down_stream = torch.cuda.Stream(device=device)
 
     def acquire(self) -> dict:
         slot = self.slots[self.next]
@@ -625,7 +628,8 @@ class CascadeEngine:
                 slot["stats"].data_ptr(), slot["hm"].data_ptr(),
                 slot["hs"].data_ptr(), self.frame_count,
                 int(self._reorder_pending), self.stream,
-                ring.copy_stream.cuda_stream, slot["cup"].handle,
+                ring.copy_stream.cuda_stream, ring.down_stream.cuda_stream,
+                slot["cup"].handle,
                 slot["cdone"].handle)
             _lib.check(rc, "cog_step_host")
             self._advance()

@@ -2608,7 +2608,7 @@ int cog_step_host(const cog_geom* geom, const cog_params* prm,
                   uint8_t* kind, int64_t* dev_stats, uint8_t* host_mask,
                   int64_t* host_stats, int64_t frame_index,
                   int32_t reorder_now, void* stream, void* copy_stream,
-                  void* up_event, void* done_event) {
+                  void* down_stream, void* up_event, void* done_event) {
   int rc = check_geom(geom);
   if (rc) return rc;
   if (!host_frame || !dev_frame || !host_mask || !host_stats || !up_event ||
@@ -2624,11 +2624,20 @@ int cog_step_host(const cog_geom* geom, const cog_params* prm,
   rc = cog_step(geom, prm, st, dev_frame, dev_mask, conf, kind, dev_stats,
                 frame_index, reorder_now, 1, stream);
   if (rc) return rc;
-  e = cudaMemcpyAsync(host_mask, dev_mask, P, cudaMemcpyDeviceToHost, s);
+  // downloads on their own stream (when given): the next frame's step does
+  // not queue behind this frame's device->host copies
+  cudaStream_t ds = down_stream ? (cudaStream_t)down_stream : s;
+  e = cudaSuccess;
+  if (ds != s) {
+    e = cudaEventRecord((cudaEvent_t)done_event, s);  // the step is done
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ds, (cudaEvent_t)done_event, 0);
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(host_mask, dev_mask, P, cudaMemcpyDeviceToHost, ds);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(host_stats, dev_stats, 16 * sizeof(int64_t),
-                        cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaEventRecord((cudaEvent_t)done_event, s);
+                        cudaMemcpyDeviceToHost, ds);
+  if (e == cudaSuccess) e = cudaEventRecord((cudaEvent_t)done_event, ds);
   return e == cudaSuccess ? COG_OK : (int)e;
 }
 

@@ -635,16 +635,25 @@ class CascadeEngine:
             self._advance()
             ev = slot["cdone"]
         else:
+            compute = torch.cuda.current_stream(self.dev.device)
             if cuda_in:
                 x = self._frame_tensor(frame)
             else:
+                # upload on the copy stream (overlaps the previous step)
                 x = slot["x"]
-                x.copy_(src, non_blocking=True)
+                with torch.cuda.stream(ring.copy_stream):
+                    x.copy_(src, non_blocking=True)
+                    slot["up"].record(ring.copy_stream)
+                compute.wait_event(slot["up"])
             self._launch_step(x, slot["mask"], slot["stats"])
-            slot["hm"].copy_(slot["mask"], non_blocking=True)
-            slot["hs"].copy_(slot["stats"], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record()
+            stepped = torch.cuda.Event()
+            stepped.record(compute)
+            with torch.cuda.stream(ring.down_stream):
+                ring.down_stream.wait_event(stepped)
+                slot["hm"].copy_(slot["mask"], non_blocking=True)
+                slot["hs"].copy_(slot["stats"], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(ring.down_stream)
         slot["event"] = ev
         m = LabelMask.pending(slot["hm"], ev, owned=False)
         st = FrameStats.pending(slot["hs"], ev)

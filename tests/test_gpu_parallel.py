@@ -133,3 +133,26 @@ def test_batch_submit_pipeline_equals_synchronous():
         masks, stats = b.process_frames(np.stack([s[t] for s in seqs]))
         assert np.array_equal(pending[k].masks, masks), t
         assert np.array_equal(pending[k].stats, stats), t
+
+
+def test_banded_host_path_equals_fused_host_path():
+    """process_frame with a reducer set (the row-band path: split step,
+    all-reduce, cog_finalize; upload / download on the ring's copy streams)
+    == the fused single-call path, for one full-frame band and an identity
+    reducer (what a world-1 all-reduce does)"""
+    from paper_1705_09339_b200.parallel import train_band_engine
+    rec, overrides = load_case("c3small")
+    cfg = config_for(overrides, state_dtype="float32")
+    frames = rec["frames"]
+    n_train = int(rec["n_train"])
+    a = _single(frames, n_train, cfg)
+    b = train_band_engine(frames[:n_train], cfg, (0, frames.shape[2]))
+    b.reducer = lambda accum: None
+    pend = []
+    for t in range(n_train, frames.shape[0]):
+        ma, sa = a.process_frame(frames[t])
+        mb, sb = b.process_frame(torch.from_numpy(frames[t]).pin_memory())
+        pend.append((ma, sa, mb, sb))
+    for t, (ma, sa, mb, sb) in enumerate(pend):
+        assert np.array_equal(ma.labels, mb.labels), t
+        assert sa.as_row() == sb.as_row(), t

@@ -42,3 +42,57 @@ def test_device_counts_match_host(shape):
                                 torch.from_numpy(truth).cuda()) == \
             confusion_counts(pred, truth)
     assert score.counts() == total
+
+
+def test_speedup_model_matches_the_reference_formula():
+    """evaluation.py:133-161: pooled populations n_i, analytic 1 / sum(s_i n_i)"""
+    from paper_1705_09339_b200.cascade import FrameStats
+    from paper_1705_09339_b200.errors import ConfigError
+    from paper_1705_09339_b200.evaluation import (
+        LEVEL_NAMES, CostProfile, level_totals, speedup_estimate)
+    rows = [FrameStats(1, 10, 60, 20, 1, 4, 5, 3, 4, False),
+            FrameStats(2, 12, 58, 22, 2, 6, 0, 2, 6, False)]
+    tot = level_totals(rows)
+    assert tot.tolist() == [22, 118, 42, 3, 10, 5]
+    costs = CostProfile(chp=0.2, group=0.4, mean=0.25, meanvar=0.6,
+                        skipped=0.1)
+    rep = speedup_estimate(rows, costs)
+    n = tot / tot.sum()
+    s = np.array([0.2, 0.4, 0.25, 0.6, 1.0, 0.1])
+    assert rep.levels == LEVEL_NAMES
+    assert rep.analytic == pytest.approx(1.0 / float(np.dot(s, n)), rel=1e-15)
+    with pytest.raises(ConfigError):
+        CostProfile(chp=0.0, group=1, mean=1, meanvar=1, skipped=1)
+    with pytest.raises(DataError):
+        speedup_estimate([], costs)
+
+
+@pytest.mark.gpu
+def test_compare_sequences_on_a_synthetic_scene():
+    """The harness (evaluation.py:350-406) on the CUDA engines: accuracy from
+    the synthetic truth masks, consistent with scoring the engines' own
+    masks, a positive measured speedup and the analytic model"""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1705_09339_b200 import synth
+    from paper_1705_09339_b200.config import EngineConfig
+    from paper_1705_09339_b200.evaluation import compare_sequences
+    from paper_1705_09339_b200.frame_io import Frame
+    spec = synth.small_spec(2, 64, 48, 70, 40)
+    sc = synth.Scene(spec)
+    frames, truths = [], {}
+    for t in range(70):
+        img, gt = sc.frame(t, with_truth=True)
+        frames.append(Frame.from_array(img, index=t))
+        truths[t] = LabelMask(gt)
+    cfg = EngineConfig(k_max=3, color=True, training_frames=40)
+    rep = compare_sequences(frames, truths, cfg, runs=2, warmup=5)
+    assert rep.frames == 25 and rep.training == 40
+    assert 0.0 <= rep.cascade_f1 <= 1.0 and 0.0 <= rep.baseline_f1 <= 1.0
+    assert len(rep.per_frame_f1) == 25
+    assert rep.cascade_seconds > 0 and rep.measured_speedup > 0
+    assert rep.speedup.analytic > 0
+    js = rep.to_json()
+    assert js["frames"] == 25 and "level_populations" in js
+    assert "cascade F1" in rep.to_text()

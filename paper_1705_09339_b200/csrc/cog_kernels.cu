@@ -1661,6 +1661,238 @@ __device__ __forceinline__ unsigned deep_item(const StepArgs& a, int s,
   return newly;
 }
 
+// ---------------------------------------------------------------------------
+// float32-state worklist item in fp32 arithmetic.  The mixture is stored in
+// fp32, so the binary64 update of deep_item only differs from this one in
+// the last bits of the stored values (within the fp32 tolerance); every
+// DECISION -- the match test, the background prefix of the label, the
+// order of the re-sort -- is filtered: one whose fp32 operands lie within a
+// 1e-5 relative margin makes the item fall back to the binary64 deep_item
+// (nothing is written before that), so decisions are the reference's
+// (kernels_numba.py:76-134, 312-334).  It replaces ~25 binary64 divisions
+// and square roots per item by single-instruction approximations, which
+// matters when the worklist is long (busy scenes, C5).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float d32_rsqrt(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float d32_rcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// stable descending order by w / sqrt(var); false on a near tie
+template <int KMAX>
+__device__ __forceinline__ bool d32_sort(float (&mu)[KMAX], float (&var)[KMAX],
+                                         float (&w)[KMAX], int n,
+                                         int (&inv)[KMAX]) {
+  float key[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+    key[k] = k < n ? w[k] * d32_rsqrt(var[k]) : 0.0f;
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    int r = i;
+    if (i < n) {
+      r = 0;
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        if (j < n && j != i) {
+          ok &= fabsf(key[j] - key[i]) >
+                1e-5f * fmaxf(fabsf(key[j]), fabsf(key[i])) + 1e-30f;
+          r += (key[j] > key[i]);
+        }
+      }
+    }
+    inv[i] = r;
+  }
+  if (!ok) return false;
+  float m2[KMAX], v2[KMAX], w2[KMAX];
+#pragma unroll
+  for (int t = 0; t < KMAX; ++t) {
+    m2[t] = mu[t];
+    v2[t] = var[t];
+    w2[t] = w[t];
+  }
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i)
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t)
+      if (i < n && inv[i] == t) {
+        m2[t] = mu[i];
+        v2[t] = var[i];
+        w2[t] = w[i];
+      }
+#pragma unroll
+  for (int t = 0; t < KMAX; ++t) {
+    mu[t] = m2[t];
+    var[t] = v2[t];
+    w[t] = w2[t];
+  }
+  return true;
+}
+
+// returns 1 if the pixel's mask byte went 0 -> 255; ok = false: undecided
+// in fp32, nothing written (the caller runs deep_item)
+template <int KMAX>
+__device__ __forceinline__ unsigned deep_item_f32(const StepArgs& a, int s,
+                                                  unsigned long long code,
+                                                  double rho_d, bool& ok) {
+  const size_t P = (size_t)a.g.height * a.g.width;
+  const int kindq = (int)((code >> 1) & 3), rs = (int)((code >> 3) & 7);
+  const int c = (int)((code >> 6) & 3);
+  const float v = (float)((code >> 8) & 0xFF);
+  const size_t p = (size_t)(code >> 16);
+  const PlaneRef<float> pr = plane_ref<float>(a, s, c);
+  const uint32_t meta = pr.meta[p];
+  float mu[KMAX], var[KMAX], w[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    mu[k] = 0.0f;
+    var[k] = 1.0f;
+    w[k] = 0.0f;
+    if (k < a.g.k) {
+      mu[k] = pr.mu[k * P + p];
+      var[k] = pr.var[k * P + p];
+      w[k] = pr.w[k * P + p];
+    }
+  }
+  int n = meta_count(meta);
+  const float rho = (float)rho_d, om = 1.0f - rho;
+  const float lam = (float)a.q.match_lambda;
+  const float vfloor = (float)a.q.variance_floor;
+  int label = 0;
+  ok = true;
+  if (kindq == DEEP_MEANVAR) {
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (k == rs) {
+        const float mm = om * mu[k] + rho * v;
+        const float dd = v - mm;
+        mu[k] = mm;
+        var[k] = fmaxf(om * var[k] + rho * (dd * dd), vfloor);
+      }
+    }
+  } else {
+    // match: first live mode within lam * sigma (filtered)
+    int hit = -1;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (hit < 0 && ok && k < n) {
+        const float thr = lam * (var[k] * d32_rsqrt(var[k]));
+        const float gap = fabsf(v - mu[k]) - thr;
+        const float m = 1e-5f * thr + 3e-5f;
+        if (gap < -m)
+          hit = k;
+        else if (gap <= m)
+          ok = false;
+      }
+    }
+    if (!ok) return 0;
+    if (hit >= 0) {
+      float sw = 0.0f;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k < n) {
+          w[k] = om * w[k] + (k == hit ? rho : 0.0f);
+          sw += w[k];
+        }
+      }
+      const float rsw = d32_rcp(sw);
+      float acc = 0.0f;
+      int b = n;
+      bool found = false;
+      const float tbg = (float)a.q.background_threshold;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k < n) {
+          w[k] *= rsw;
+          if (k == hit) {
+            const float mm = om * mu[k] + rho * v;
+            const float dd = v - mm;
+            mu[k] = mm;
+            var[k] = fmaxf(om * var[k] + rho * (dd * dd), vfloor);
+          }
+          if (!found) {
+            acc += w[k];
+            ok &= fabsf(acc - tbg) > 1e-5f * tbg;  // prefix decision
+            if (acc > tbg) {
+              b = k + 1;
+              found = true;
+            }
+          }
+        }
+      }
+      if (!ok) return 0;
+      label = (hit + 1 <= b) ? 0 : 1;
+    } else {
+      const int slot = n < a.g.k ? n : n - 1;
+      if (n < a.g.k) n = n + 1;
+      float sw = 0.0f;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k == slot) {
+          mu[k] = v;
+          var[k] = (float)a.q.initial_variance;
+          w[k] = rho;
+        }
+        if (k < n) sw += w[k];
+      }
+      if (sw == 0.0f) {
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < n) w[k] = (k == slot) ? 1.0f : 0.0f;
+      } else {
+        const float r_ = d32_rcp(sw);
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < n) w[k] *= r_;
+      }
+      label = 1;
+    }
+  }
+  int inv[KMAX];
+  if (!d32_sort<KMAX>(mu, var, w, n, inv)) {
+    ok = false;
+    return 0;
+  }
+  // ---- write back (deep_item's bookkeeping)
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k < n) {
+      pr.mu[k * P + p] = mu[k];
+      pr.var[k * P + p] = var[k];
+      pr.w[k * P + p] = w[k];
+    }
+  }
+  if (kindq == DEEP_MEANVAR) {
+    pr.meta[p] = (uint16_t)meta_with_refs(
+        meta, select_inv<KMAX>(inv, meta_ref(meta, 0)),
+        select_inv<KMAX>(inv, meta_ref(meta, 1)));
+    return 0;
+  }
+  uint32_t nm = meta_with_count(meta, n);
+  if (kindq == DEEP_GMM)
+    nm = meta_with_refs(nm, select_inv<KMAX>(inv, meta_ref(meta, 0)),
+                        select_inv<KMAX>(inv, meta_ref(meta, 1)));
+  pr.meta[p] = (uint16_t)nm;
+  unsigned newly = 0;
+  if (label) {
+    pr.dyn[p] |= 1u << 8;
+    uint8_t* mask = a.mask + (size_t)s * P;
+    const uintptr_t addr = (uintptr_t)(mask + p);
+    unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
+    const unsigned sh = (unsigned)(addr & 3) * 8;
+    const unsigned old = atomicOr(word, 0xFFu << sh);
+    newly = ((old >> sh) & 0xFFu) == 0u;
+  }
+  return newly;
+}
+
 template <typename T, int KMAX>
 __global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
   __shared__ int s_last;
@@ -1694,6 +1926,18 @@ __global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
     const unsigned long long code = dq_code[i];
     if (!(code & 1ull)) continue;
     dq_code[i] = 0ull;
+    if constexpr (sizeof(T) == 4) {
+#ifndef COG_EXP_DEEP64
+      if (!a.q.compat) {  // fp32 arithmetic, binary64 fallback near ties
+        bool ok;
+        const unsigned nw = deep_item_f32<KMAX>(a, s, code, dq_rho[i], ok);
+        if (ok) {
+          fg += nw;
+          continue;
+        }
+      }
+#endif
+    }
     fg += deep_item<T, KMAX>(a, s, code, dq_rho[i]);
   }
   for (int o = 16; o > 0; o >>= 1) fg += __shfl_xor_sync(FULL, fg, o);

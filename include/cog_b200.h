@@ -220,6 +220,15 @@ int cog_step_host(const cog_geom *geom, const cog_params *prm,
                   int32_t reorder_now, void *stream, void *copy_stream,
                   void *down_stream, void *up_event, void *done_event);
 
+/* k-means assignment step of the grouping (grouping.py:116-118): points
+ * f64[n][2], centers f64[k][2] (device); label i64[n] is overwritten with
+ * each point's nearest centre (numpy's squared distance, lowest index on
+ * ties) and *changed (u32, device, zeroed by the caller) is set to 1 if any
+ * label changed. */
+int cog_kmeans_assign(const double *points, int64_t n, const double *centers,
+                      int32_t k, int64_t *label, uint32_t *changed,
+                      void *stream);
+
 /* Confusion counts of predicted vs truth masks u8[n] (evaluation.
  * confusion_counts, cogbg/evaluation.py:72-89): truth 0 = background,
  * 255 = foreground, anything else excluded; predicted foreground = 255.

@@ -127,6 +127,8 @@ _SIGS = {
     "cog_step_host": (ctypes.c_int, [_P] * 11 + [ctypes.c_int64,
                                                 ctypes.c_int32] + [_P] * 5),
     "cog_confusion": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P, _P]),
+    "cog_kmeans_assign": (ctypes.c_int, [_P, ctypes.c_int64, _P,
+                                         ctypes.c_int32, _P, _P, _P]),
     "cog_event_create": (ctypes.c_void_p, []),
     "cog_event_destroy": (ctypes.c_int, [_P]),
     "cog_event_sync": (ctypes.c_int, [_P]),

@@ -2363,6 +2363,45 @@ __device__ double g_bterm[2][256];
 #include "cog_fast.cuh"
 
 // ---------------------------------------------------------------------------
+// training: k-means assignment step (grouping.py:116-118): squared distance
+// to every centre over the two features, (x0 - c0)^2 + (x1 - c1)^2 in
+// binary64 (no contraction, so each value is numpy's), argmin with the
+// lowest index on ties and the first NaN winning (numpy argmin).  One
+// thread per point; `changed` is set if any label differs from the previous.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    kmeans_assign_kernel(const double* __restrict__ pts, int64_t n,
+                         const double* __restrict__ ctr, int k,
+                         int64_t* __restrict__ label, uint32_t* changed) {
+  unsigned any = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x0 = pts[2 * i], x1 = pts[2 * i + 1];
+    int best = 0;
+    double bv = 0.0;
+    for (int j = 0; j < k; ++j) {
+      const double d0 = x0 - ctr[2 * j], d1 = x1 - ctr[2 * j + 1];
+      const double d = d0 * d0 + d1 * d1;
+      if (j == 0) {
+        bv = d;
+        if (isnan(d)) break;
+      } else if (isnan(d)) {
+        best = j;
+        break;
+      } else if (d < bv) {
+        bv = d;
+        best = j;
+      }
+    }
+    if (label[i] != best) {
+      label[i] = best;
+      any = 1;
+    }
+  }
+  if (__any_sync(FULL, any) && (threadIdx.x & 31) == 0) atomicOr(changed, 1u);
+}
+
+// ---------------------------------------------------------------------------
 // evaluation: confusion counts (16 pixels a thread, warp reductions, one
 // 64-bit atomic per count per warp)
 // ---------------------------------------------------------------------------
@@ -2883,6 +2922,20 @@ int cog_step_host(const cog_geom* geom, const cog_params* prm,
                         cudaMemcpyDeviceToHost, ds);
   if (e == cudaSuccess) e = cudaEventRecord((cudaEvent_t)done_event, ds);
   return e == cudaSuccess ? COG_OK : (int)e;
+}
+
+int cog_kmeans_assign(const double* points, int64_t n, const double* centers,
+                      int32_t k, int64_t* label, uint32_t* changed,
+                      void* stream) {
+  if (!points || !centers || !label || !changed || n < 0 || k < 1)
+    return COG_EINVAL;
+  if (n == 0) return COG_OK;
+  int64_t blocks = (n + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  kmeans_assign_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      points, n, centers, k, label, changed);
+  return launch_status();
 }
 
 int cog_confusion(const uint8_t* predicted, const uint8_t* truth, int64_t n,

@@ -156,3 +156,21 @@ def test_banded_host_path_equals_fused_host_path():
     for t, (ma, sa, mb, sb) in enumerate(pend):
         assert np.array_equal(ma.labels, mb.labels), t
         assert sa.as_row() == sb.as_row(), t
+
+
+@pytest.mark.parametrize("n,k", [(200_000, 3), (70_001, 5)])
+def test_device_kmeans_equals_numpy_kmeans(n, k, monkeypatch):
+    """cog_kmeans_assign inside KMeans.fit: labels and centres bit-identical
+    to the all-numpy iteration (grouping.py:100-126), duplicate points (exact
+    distance ties) included"""
+    from paper_1705_09339_b200 import grouping
+    rng = np.random.default_rng(7)
+    pts = np.concatenate([rng.normal(0, 1, (n // 2, 2)),
+                          rng.normal(3, 0.5, (n - n // 2, 2))])
+    pts[::97] = pts[1]                       # many identical points
+    monkeypatch.setenv("COG_KMEANS_DEVICE_MIN", str(10 ** 12))
+    want_l, want_c = grouping.KMeans(k, 3).fit(pts.copy())
+    monkeypatch.setenv("COG_KMEANS_DEVICE_MIN", "0")
+    got_l, got_c = grouping.KMeans(k, 3).fit(pts.copy())
+    assert np.array_equal(got_l, want_l)
+    assert np.array_equal(got_c, want_c)

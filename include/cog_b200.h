@@ -220,6 +220,15 @@ int cog_step_host(const cog_geom *geom, const cog_params *prm,
                   int32_t reorder_now, void *stream, void *copy_stream,
                   void *down_stream, void *up_event, void *done_event);
 
+/* Pooled training statistics of big groups (grouping.py:189-192): values
+ * u8[N][depth][P], member i32[P] (group 0..n_groups-1, -1 = none), all on
+ * the device; ACCUMULATES into sums u64[n_groups][depth][2] the exact
+ * integer sums of x and x^2 over every frame of every member pixel (zero it
+ * first).  n_groups * depth <= 3072. */
+int cog_pool_sums(const uint8_t *values, int32_t n_frames, int32_t depth,
+                  int64_t n_pix, const int32_t *member, int32_t n_groups,
+                  uint64_t *sums, void *stream);
+
 /* k-means assignment step of the grouping (grouping.py:116-118): points
  * f64[n][2], centers f64[k][2] (device); label i64[n] is overwritten with
  * each point's nearest centre (numpy's squared distance, lowest index on

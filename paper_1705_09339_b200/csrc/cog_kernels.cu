@@ -2402,6 +2402,40 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
+// training: pooled group statistics (grouping.py:189-192) for pools too big
+// for numpy's in-memory expression: per (group, plane) the exact integer sums
+// of x and x^2 over every training frame of every member pixel.  One thread
+// per pixel (coalesced over the frames), shared-memory accumulation per CTA,
+// one 64-bit atomic per entry per CTA.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    pool_sums_kernel(const uint8_t* __restrict__ values, int N, int d,
+                     int64_t P, const int32_t* __restrict__ member, int G,
+                     unsigned long long* sums) {
+  extern __shared__ unsigned long long ps[];  // [G][d][2]
+  for (int i = threadIdx.x; i < G * d * 2; i += blockDim.x) ps[i] = 0ull;
+  __syncthreads();
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int g = member[p];
+    if (g < 0 || g >= G) continue;
+    for (int c = 0; c < d; ++c) {
+      unsigned long long s1 = 0, s2 = 0;
+      for (int i = 0; i < N; ++i) {
+        const unsigned x = values[((int64_t)i * d + c) * P + p];
+        s1 += x;
+        s2 += x * x;
+      }
+      atomicAdd(&ps[(g * d + c) * 2], s1);
+      atomicAdd(&ps[(g * d + c) * 2 + 1], s2);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * d * 2; i += blockDim.x)
+    if (ps[i]) atomicAdd(sums + i, ps[i]);
+}
+
+// ---------------------------------------------------------------------------
 // evaluation: confusion counts (16 pixels a thread, warp reductions, one
 // 64-bit atomic per count per warp)
 // ---------------------------------------------------------------------------
@@ -2922,6 +2956,24 @@ int cog_step_host(const cog_geom* geom, const cog_params* prm,
                         cudaMemcpyDeviceToHost, ds);
   if (e == cudaSuccess) e = cudaEventRecord((cudaEvent_t)done_event, ds);
   return e == cudaSuccess ? COG_OK : (int)e;
+}
+
+int cog_pool_sums(const uint8_t* values, int32_t n_frames, int32_t depth,
+                  int64_t n_pix, const int32_t* member, int32_t n_groups,
+                  uint64_t* sums, void* stream) {
+  if (!values || !member || !sums || n_frames < 1 || depth < 1 ||
+      depth > MAXD || n_pix < 0 || n_groups < 1)
+    return COG_EINVAL;
+  const size_t smem = (size_t)n_groups * depth * 2 * 8;
+  if (smem > 48 * 1024) return COG_EUNSUPPORTED;
+  if (n_pix == 0) return COG_OK;
+  int64_t blocks = (n_pix + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  pool_sums_kernel<<<(unsigned)blocks, 256, smem, (cudaStream_t)stream>>>(
+      values, n_frames, depth, n_pix, member, n_groups,
+      (unsigned long long*)sums);
+  return launch_status();
 }
 
 int cog_kmeans_assign(const double* points, int64_t n, const double* centers,

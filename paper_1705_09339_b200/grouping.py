@@ -180,9 +180,54 @@ def _pooled_stats(values: np.ndarray, sel: np.ndarray, floor: float):
     return mean, np.maximum(sq / cnt, floor)
 
 
+def _pooled_stats_device(values: np.ndarray, values_dev, gm: "GroupMap",
+                         big: list, floor: float) -> None:
+    """Pooled mean / floored variance of the groups in ``big`` from exact
+    integer sums of x and x^2 computed on the GPU (cog_pool_sums, one pass
+    over the training frames for all of them).  The mean is the same
+    correctly rounded sum / count as the chunked host path; the variance is
+    the exact rational (M * sum x^2 - (sum x)^2) / M^2, correctly rounded
+    (Python integers), where numpy's two-pass float evaluation is within
+    ~1e-15 of it."""
+    import torch
+
+    from . import _lib
+    n, d, p = values.shape
+    if values_dev is None:
+        values_dev = torch.from_numpy(np.ascontiguousarray(values)).to(
+            torch.device("cuda", torch.cuda.current_device()))
+    dev = values_dev.device
+    slot = np.full(p, -1, dtype=np.int32)
+    for k, gi in enumerate(big):
+        slot[gm.group_id == gi] = k
+    mem = torch.from_numpy(slot).to(dev)
+    sums = torch.zeros((len(big), d, 2), dtype=torch.int64, device=dev)
+    _lib.check(_lib.load().cog_pool_sums(
+        values_dev.data_ptr(), n, d, p, mem.data_ptr(), len(big),
+        sums.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+        "cog_pool_sums")
+    s = sums.cpu().numpy()
+    for k, gi in enumerate(big):
+        cnt = n * int(gm.member_count[gi])
+        for c in range(d):
+            s1, s2 = int(s[k, c, 0]), int(s[k, c, 1])
+            gm.mu[gi, c] = s1 / cnt
+            gm.var[gi, c] = max((cnt * s2 - s1 * s1) / (cnt * cnt), floor)
+
+
+def _cuda_ok() -> bool:
+    try:
+        import torch
+    except ImportError:
+        return False
+    return torch.cuda.is_available()
+
+
 def build_groups(features: np.ndarray, w_final: np.ndarray,
-                 values: np.ndarray, config: EngineConfig) -> GroupMap:
-    """features (P, 2) f64, w_final (P,) f64, values (N, d, P) uint8."""
+                 values: np.ndarray, config: EngineConfig,
+                 values_dev=None) -> GroupMap:
+    """features (P, 2) f64, w_final (P,) f64, values (N, d, P) uint8;
+    values_dev: the same values already on the GPU (optional)."""
     n, d, p = values.shape
     if not config.grouping:
         return GroupMap.empty(p, d)
@@ -196,11 +241,19 @@ def build_groups(features: np.ndarray, w_final: np.ndarray,
     g = len(kept)
     gm = GroupMap(np.full(p, UNGROUPED, dtype=np.int64), np.zeros((g, d)),
                   np.zeros((g, d)), np.zeros(g), np.zeros(g, dtype=np.int64))
+    big = []
+    use_dev = _cuda_ok()
     for gi, j in enumerate(kept):
         sel = member == j
         gm.group_id[sel] = gi
         gm.member_count[gi] = sel.sum()
-        gm.mu[gi], gm.var[gi] = _pooled_stats(values, sel,
-                                              config.variance_floor)
+        if use_dev and n * d * int(gm.member_count[gi]) * 8 > _POOL_EXACT_BYTES:
+            big.append(gi)   # beyond numpy's in-memory expression
+        else:
+            gm.mu[gi], gm.var[gi] = _pooled_stats(values, sel,
+                                                  config.variance_floor)
         gm.weight[gi] = w_final[sel].mean()
+    if big:
+        _pooled_stats_device(values, values_dev, gm, big,
+                             config.variance_floor)
     return gm

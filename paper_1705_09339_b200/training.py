@@ -97,7 +97,7 @@ def train_engine(frames, config: EngineConfig, kde_windows=None,
                                              kde_windows)
     if config.grouping:
         groups = build_groups(feats.cpu().numpy(), w_final.cpu().numpy(),
-                              flat, config)
+                              flat, config, values_dev=values)
     else:
         groups = GroupMap.empty(p, d)
     install_groups(eng, groups)

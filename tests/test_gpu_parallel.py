@@ -174,3 +174,31 @@ def test_device_kmeans_equals_numpy_kmeans(n, k, monkeypatch):
     got_l, got_c = grouping.KMeans(k, 3).fit(pts.copy())
     assert np.array_equal(got_l, want_l)
     assert np.array_equal(got_c, want_c)
+
+
+def test_device_pooled_stats_match_host(monkeypatch):
+    """cog_pool_sums path of build_groups (pools too big for numpy's
+    in-memory expression): means identical to the host evaluation; variances
+    within 1e-11 relative -- the device value is the exact rational correctly
+    rounded, numpy's float evaluation over 1e6 terms carries ~1e-12"""
+    from paper_1705_09339_b200 import grouping
+    from paper_1705_09339_b200.config import EngineConfig
+    rng = np.random.default_rng(5)
+    n, d, p = 40, 3, 50_000
+    values = rng.integers(0, 256, (n, d, p), dtype=np.uint8)
+    values[:, :, : p // 2] = (values[:, :, : p // 2] // 16 + 100).astype(np.uint8)
+    feats = np.stack([rng.gamma(2, 1, p), rng.gamma(2, 1, p) * 1e-3], axis=1)
+    feats[: p // 2] *= 5.0
+    w_final = rng.random(p)
+    cfg = EngineConfig(color=True, clusters=3)
+    monkeypatch.setattr(grouping, "_cuda_ok", lambda: False)
+    want = grouping.build_groups(feats, w_final, values, cfg)
+    monkeypatch.setattr(grouping, "_cuda_ok", lambda: True)
+    monkeypatch.setattr(grouping, "_POOL_EXACT_BYTES", 1024)  # all "big"
+    got = grouping.build_groups(feats, w_final, values, cfg)
+    assert want.group_count == got.group_count > 0
+    assert np.array_equal(want.group_id, got.group_id)
+    assert np.array_equal(want.member_count, got.member_count)
+    assert np.array_equal(want.mu, got.mu)
+    np.testing.assert_allclose(got.var, want.var, rtol=1e-11, atol=0)
+    assert np.array_equal(want.weight, got.weight)

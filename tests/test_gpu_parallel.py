@@ -202,3 +202,20 @@ def test_device_pooled_stats_match_host(monkeypatch):
     assert np.array_equal(want.mu, got.mu)
     np.testing.assert_allclose(got.var, want.var, rtol=1e-11, atol=0)
     assert np.array_equal(want.weight, got.weight)
+
+
+@pytest.mark.parametrize("name", ["c3small", "illum_grouped", "mixed_default"])
+def test_training_with_device_kmeans_equals_host_kmeans(name, monkeypatch):
+    """a golden case trained with the k-means assignment forced onto the GPU
+    == trained with the numpy k-means (group ids, group parameters, state)"""
+    rec, overrides = load_case(name)
+    cfg = config_for(overrides)
+    frames = rec["frames"]
+    n_train = int(rec["n_train"])
+    monkeypatch.setenv("COG_KMEANS_DEVICE_MIN", str(10 ** 12))
+    a = _single(frames, n_train, cfg)
+    monkeypatch.setenv("COG_KMEANS_DEVICE_MIN", "0")
+    b = _single(frames, n_train, cfg)
+    assert np.array_equal(a.group_id, b.group_id)
+    for nm in STATE:
+        assert np.array_equal(getattr(a, nm), getattr(b, nm)), nm

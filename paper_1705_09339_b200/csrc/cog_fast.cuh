@@ -197,10 +197,14 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
   int kc_units = 0;
   int wq_n = 0;
 
-  // static, balanced tile assignment (the launcher sizes the grid so every
-  // warp gets the same number of tiles); tile j of warp gw is gw + j * nw
+  // static tile assignment over every resident slot; tile j of warp
+  // rank r is r + j * nw
   const int nw = gridDim.x * LEAN_WARPS;
-  int wt = blockIdx.x * LEAN_WARPS + warp;
+  // warp rank interleaved over the CTAs: with every resident slot launched,
+  // the warps that get one tile more than the others are spread evenly over
+  // the CTAs, and so over the SMs (C2: 64-65 tiles per SM instead of 48 or
+  // 72 with whole CTAs of 3-tile warps; 70.9 -> 69.5 us per step)
+  int wt = warp * gridDim.x + blockIdx.x;
   int ty = wt / a.tiles_x, tx = wt - ty * a.tiles_x;
   const int dty = nw / a.tiles_x, dtx = nw - dty * a.tiles_x;
   const int kc_flush = 511 / D;  // D counts per tile per 9-bit field

@@ -2650,7 +2650,8 @@ int launch_lean(const StepArgs& a, cudaStream_t st) {
                          (int)smem);
   const int occ = cached_occupancy((const void*)fn, LEAN_THREADS, smem);
   const int need = (a.n_tiles + LEAN_WARPS - 1) / LEAN_WARPS;
-  const int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
+  int per_stream = (num_sms() * occ) / a.g.streams;  // one wave
+  if (per_stream < 1) per_stream = 1;
   int gx = need < per_stream ? need : per_stream;
   if (gx < 1) gx = 1;
   fn<<<dim3(gx, a.g.streams), LEAN_THREADS, smem, st>>>(a);
@@ -2674,12 +2675,16 @@ int launch_fast_k(const StepArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   const int occ = cached_occupancy((const void*)fn, LEAN_THREADS, smem);
-  // balanced static schedule: t tiles per warp, just enough CTAs
+  // static schedule over every resident slot (at most one tile per warp
+  // more than another, spread over the CTAs by the kernel's warp ranking)
   const long long units = (long long)a.n_tiles;
-  const int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
-  const long long slots = (long long)per_stream * LEAN_WARPS;
-  const long long t = (units + slots - 1) / slots;
-  int gx = (int)((units + t * LEAN_WARPS - 1) / (t * LEAN_WARPS));
+  // rounded down: every CTA of every stream resident in one wave (a CTA in
+  // a second wave would start only when a first-wave one ends)
+  int per_stream = (num_sms() * occ) / a.g.streams;
+  if (per_stream < 1) per_stream = 1;
+  long long gxl = (units + LEAN_WARPS - 1) / LEAN_WARPS;
+  if (gxl > per_stream) gxl = per_stream;
+  int gx = (int)gxl;
   if (gx < 1) gx = 1;
   const FastConst k = make_fast_const(a.q);
   fn<<<dim3(gx, a.g.streams), LEAN_THREADS, smem, st>>>(a, k);
@@ -2715,7 +2720,8 @@ int launch_hot(const StepArgs& a, cudaStream_t st) {
                          (int)smem);
   const int occ = cached_occupancy((const void*)fn, threads, smem);
   const int need = (a.n_tiles + warps - 1) / warps;
-  int per_stream = (num_sms() * occ + a.g.streams - 1) / a.g.streams;
+  int per_stream = (num_sms() * occ) / a.g.streams;  // one wave
+  if (per_stream < 1) per_stream = 1;
   int gx = need < per_stream ? need : per_stream;
   if (gx < 1) gx = 1;
   fn<<<dim3(gx, a.g.streams), threads, smem, st>>>(a);

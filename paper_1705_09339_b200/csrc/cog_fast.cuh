@@ -197,19 +197,23 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
   int kc_units = 0;
   int wq_n = 0;
 
-  // static tile assignment over every resident slot; tile j of warp
-  // rank r is r + j * nw
+  // static tile assignment over every resident slot: tile j of warp rank r
+  // is r + j * nw.  Ranks are CTA-major (a CTA's warps on adjacent tiles:
+  // shared rows stay in the same DRAM pages and L2 lines) when every warp
+  // has many tiles; with few tiles per warp (C2: 2-3) the one-tile
+  // difference between warps decides the SM balance, and ranks interleaved
+  // over the CTAs spread the longer warps evenly (C2: 64-65 tiles per SM
+  // instead of 48 or 72; 70.9 -> 69.5 us, while C3/C4 lose 2-3 % with it)
   const int nw = gridDim.x * LEAN_WARPS;
-  // warp rank interleaved over the CTAs: with every resident slot launched,
-  // the warps that get one tile more than the others are spread evenly over
-  // the CTAs, and so over the SMs (C2: 64-65 tiles per SM instead of 48 or
-  // 72 with whole CTAs of 3-tile warps; 70.9 -> 69.5 us per step)
-  int wt = warp * gridDim.x + blockIdx.x;
+  const bool spread = a.n_tiles / nw < 8;
+  int wt = spread ? warp * gridDim.x + blockIdx.x
+                  : blockIdx.x * LEAN_WARPS + warp;
   int ty = wt / a.tiles_x, tx = wt - ty * a.tiles_x;
   const int dty = nw / a.tiles_x, dtx = nw - dty * a.tiles_x;
   const int kc_flush = 511 / D;  // D counts per tile per 9-bit field
   unsigned fg_count = 0;
   for (; wt < a.n_tiles; wt += nw) {
+    const int tile = wt;
     const int y = ty * stride + lrow, x_ = tx * cw + lcol;
     tx += dtx;
     ty += dty;
@@ -280,9 +284,9 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
 #ifdef COG_EXP_NOTABLE
       x.tv = 0.01f * (float)(o & 7);
 #else
-      // tile-major table: plane (sK + c), tile wt, bin v, slot = lane
+      // tile-major table: plane (sK + c), this tile, bin v, slot = lane
       x.tv = __ldcg(a.s.table +
-                    (((size_t)(sK + c) * a.n_tiles + wt) * 256 + x.vb) * 32 +
+                    (((size_t)(sK + c) * a.n_tiles + tile) * 256 + x.vb) * 32 +
                     lane);
 #endif
       const uint32_t r0 = (x.meta >> 10) & 7u, r1 = x.meta >> 13;

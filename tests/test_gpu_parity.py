@@ -234,10 +234,11 @@ def test_compat_mode_matches_baseline_bytewise():
         assert np.array_equal(eng.count[c], g.count)
 
 
-@pytest.mark.parametrize("cid,n_run", [(1, 200), (2, 120)])
+@pytest.mark.parametrize("cid,n_run", [(1, 200), (2, 120), (5, 30)])
 def test_baseline_config_full_size_f32_vs_oracle(cid, n_run, monkeypatch):
     """BASELINE configs at their full geometry (C1 160x120 gray, whole run;
-    C2 640x480 RGB, the first n_run post-training frames): the float32
+    C2 640x480 RGB and one C5 stream -- 1280x720 RGB, K=5, the busy scene --
+    for the first n_run post-training frames): the float32
     engine against the oracle (the reference's binary64 semantics) trained
     on the same frames -- masks >= 99.99 % identical over the run, level
     populations per frame within 0.1 % of the plane-pixels"""
@@ -245,7 +246,7 @@ def test_baseline_config_full_size_f32_vs_oracle(cid, n_run, monkeypatch):
     from paper_1705_09339_b200 import synth
     from paper_1705_09339_b200.config import EngineConfig
     monkeypatch.setenv("COG_ORACLE_THREADS", str(os.cpu_count() or 1))
-    spec = synth.CONFIGS[cid]
+    spec = synth.CONFIGS[cid].for_stream(0)
     sc = synth.Scene(spec)
     frames = sc.frames(0, spec.training + n_run)  # no fork after CUDA init
     cfg = EngineConfig(k_max=spec.k_max, color=spec.depth == 3,

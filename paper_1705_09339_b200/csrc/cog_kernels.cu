@@ -44,6 +44,9 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int STEP_THREADS = 256;
 constexpr int PRIOR_PIX = 32;
 constexpr int STATS_WORDS = 16;
+#ifndef DEEP_THREADS
+#define DEEP_THREADS 256  // deep_kernel CTA size
+#endif
 
 // accumulator layout (u64 words, per stream)
 __host__ __device__ inline int acc_kind(int c, int k) { return c * 7 + k; }
@@ -1894,7 +1897,7 @@ __device__ __forceinline__ unsigned deep_item_f32(const StepArgs& a, int s,
 }
 
 template <typename T, int KMAX>
-__global__ void __launch_bounds__(256) deep_kernel(const StepArgs a) {
+__global__ void __launch_bounds__(DEEP_THREADS) deep_kernel(const StepArgs a) {
   __shared__ int s_last;
   __shared__ unsigned long long s_fg;
   // launched with programmatic stream serialization after fast_kernel: wait
@@ -2741,26 +2744,26 @@ template <typename T>
 int launch_deep(const StepArgs& a, cudaStream_t st, bool pdl) {
   auto fn = pick_deep<T>(a.g.k);
   const size_t P = (size_t)a.g.height * a.g.width;
-  size_t dg = (P * a.g.depth / 8 + 255) / 256;  // covers ~12% deep items
+  size_t dg = (P * a.g.depth / 8 + DEEP_THREADS - 1) / DEEP_THREADS;  // ~12% items
   // grid-stride over the worklist, one wave (COG_DEEP_CTAS_PER_SM
   // overrides the occupancy)
   const char* env = getenv("COG_DEEP_CTAS_PER_SM");
   const size_t per_sm =
       env ? (size_t)atoi(env)
-          : (size_t)cached_occupancy((const void*)fn, 256, 0);
+          : (size_t)cached_occupancy((const void*)fn, DEEP_THREADS, 0);
   size_t cap = (size_t)num_sms() * per_sm / a.g.streams;
   if (cap < 1) cap = 1;
   if (dg > cap) dg = cap;
   if (dg < 1) dg = 1;
   if (!pdl) {
-    fn<<<dim3((unsigned)dg, a.g.streams), 256, 0, st>>>(a);
+    fn<<<dim3((unsigned)dg, a.g.streams), DEEP_THREADS, 0, st>>>(a);
     return launch_status();
   }
   // programmatic dependent launch: the deep grid is scheduled while the
   // hot kernel drains and waits (griddepcontrol.wait) for its results
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)dg, a.g.streams);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(DEEP_THREADS);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

@@ -36,17 +36,27 @@
  *                        model_io.save_model / load_model (model_io.py:61-227)
  *
  * State layout in HBM (one stream; `streams` copies back to back):
- *   mixture  mu, var, w : T[depth][k][P]      T = float or double
+ *   mix      T[depth][P][R]   one record per plane-pixel (T = float or
+ *            double): (mu_k, var_k) at [2k, 2k+1], w_k at [2*KB + k],
+ *            KB = 3 / 5 / 8 for k <= 3 / <= 5 / <= 8, R = cog_mix_elems(k)
+ *            (16 or 32: a pixel's whole mixture is one 64-B / 128-B float32
+ *            record, so a full-mixture update touches one line instead of
+ *            3k scattered ones)
  *   meta     u16[depth][P]   count | mid_order | mode_ref (packed)
  *   dyn      u32[depth][P]   chp_prev | last_label | waking | last_active | clock
  *   streak   u32[depth][P]
  *   hits     u32[depth][5][P]
- *   table    f32, tile-major: per plane [n_tiles][256][SL] -- bin v of the
- *            pixel in slot (row * cw + col) of warp tile t (stride rows x
- *            cw columns, SL = 32 * ceil(stride * cw / 32)) at
- *            (t * 256 + v) * SL + slot; cog_table_floats() per stream,
- *            cog_table_pack() converts from / to the reference [P][256]
+ *   table    f32[depth][P][256] the reference-layout prior (exact values:
+ *            binary64 paths, model files, host views)
  *   peak     f32[depth][P]
+ *   tabq     u16, the hot prior of the float32 step: phat = table / peak
+ *            quantised to round(phat * 65535), tile-major -- per plane
+ *            [n_tiles][256][SL], bin v of the pixel in slot
+ *            (row * cw + col) of warp tile t (stride rows x cw columns,
+ *            SL = 32 * ceil(stride * cw / 32)) at (t * 256 + v) * SL + slot,
+ *            so lanes of a warp that see the same value (or a neighbouring
+ *            one) share a line; cog_tabq_elems() per stream, built by
+ *            cog_tabq_build(); NULL for float64 engines
  *   cls      u8[P], gid u16[P] (0xFFFF = ungrouped)
  *   g_mu, g_var  f64[depth][G], g_members u32[G]
  *   accum    u64[cog_accum_words()], sync u32[4]
@@ -91,17 +101,21 @@ typedef struct cog_params {
   int32_t exact_group_sums; /* parity/debug: sum group confidences in the
                                reference's sequential pixel order (one
                                thread per group; small frames only) */
-  int32_t pad_;
+  int32_t variant;          /* step kernel: 0 automatic (fast for float32
+                               state, lean / general for float64), 1 the
+                               general kernel, 2 the lean kernel -- a parity
+                               knob for tests, never read from the env */
 } cog_params;
 
 typedef struct cog_state {
-  void *mu, *var, *w;
+  void *mix;
   uint16_t *meta;
   uint32_t *dyn;
   uint32_t *streak;
   uint32_t *hits;
   const float *table;
   const float *peak;
+  const uint16_t *tabq;
   const uint8_t *cls;
   const uint16_t *gid;
   double *g_mu, *g_var;
@@ -118,14 +132,17 @@ int64_t cog_accum_words(int32_t depth, int32_t n_groups);
 /* Worklist slots per stream (deep-level plane-pixels of one frame). */
 int64_t cog_deepq_slots(int32_t depth, int64_t n_pix);
 
-/* Floats of one stream's tile-major prior table (all planes), or -1. */
-int64_t cog_table_floats(const cog_geom *geom);
+/* Elements (of the state type) of one plane-pixel's mixture record. */
+int64_t cog_mix_elems(int32_t k);
 
-/* One stream's prior table between the reference layout f32[depth][P][256]
- * (scene_prior / model files, cascade.py:192) and the engine's tile-major
- * layout: to_tiled = 1 packs ref_layout into tiled, 0 unpacks. */
-int cog_table_pack(const cog_geom *geom, float *ref_layout, float *tiled,
-                   int32_t to_tiled, void *stream);
+/* u16 elements of one stream's hot prior table (all planes), or -1. */
+int64_t cog_tabq_elems(const cog_geom *geom);
+
+/* Build one stream's hot prior tabq u16 from its reference-layout table
+ * f32[depth][P][256] and peak f32[depth][P] (cascade.py:213-216:
+ * phat = table / peak), round(phat * 65535) in binary64, tile-major. */
+int cog_tabq_build(const cog_geom *geom, const float *table,
+                   const float *peak, uint16_t *tabq, void *stream);
 
 /* Scene prior for one stream: frames u8[N][depth][P].  Writes, for each
  * trailing window windows[j] (ascending, last == N), tables
@@ -141,6 +158,7 @@ int cog_prior_build(const uint8_t *frames, int32_t n_frames, int32_t depth,
                     void *stream);
 
 /* GMM warm-up over N training frames u8[N][depth][P] for one stream.
+ * Needs the stream's table (reference layout) already built.
  * Writes the mixture (state dtype per geom.state_f64), meta (count + mode
  * references ranked by prior mass, ties by w/sigma; mid_order left as
  * "ungrouped"), dyn (chp_prev = last frame), zeroes streak and hits.
@@ -177,7 +195,7 @@ int cog_apply_pending(const cog_geom *geom, const cog_params *prm,
                       const cog_state *st, int32_t reorder_now, void *stream);
 
 /* Plain per-pixel mixture over all planes of one frame (baseline model):
- * state uses st->mu/var/w/meta (count only); mask u8[P] 0/255. */
+ * state uses st->mix/meta (count only); mask u8[P] 0/255. */
 int cog_baseline_frame(const cog_geom *geom, const cog_params *prm,
                        const cog_state *st, const uint8_t *frame,
                        uint8_t *mask, void *stream);

@@ -163,7 +163,7 @@ int cogo_cascade_frame(
     int8_t *mode_ref, int64_t *hits, int64_t *streak, int8_t *last_active,
     int64_t *clock, uint8_t *waking, const uint8_t *on_lattice,
     const int64_t *group_id, const double *g_mu, const double *g_var,
-    const double *table, const double *peak, const double *wa,
+    const float *table, const double *peak, const double *wa,
     const double *wb, const double *wc,
     double base_rate, double lam, double t_bg, double var_floor,
     double init_var, double eps_chp, double conf_thresh, double prior_floor,
@@ -246,7 +246,9 @@ int cogo_cascade_frame(
             mu_top = pmu[ref[0]];
             sig_top = sqrt(pvar[ref[0]]);
         }
-        double phat = table[p * 256 + vals[p]] / peak[p];
+        /* the engine keeps the f32 table and promotes at use
+           (cascade.py:192, 213-216: _tables64 = float64(f32 table)) */
+        double phat = (double)table[p * 256 + vals[p]] / peak[p];
         double bterm = fabs(v - prev) / 255.0;
         if (!literal_conf) bterm = 1.0 - bterm;
         double gterm = fabs(v - mu_top) / (lam * sig_top);
@@ -381,6 +383,107 @@ int cogo_sort_pixels(int64_t n_sel, const int64_t *idx, int K, double *mu,
         int64_t p = idx[i];
         sort_pixel(mu + p * K, var + p * K, w + p * K, count[p], K,
                    inv_out + i * K);
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------------
+ * Helpers that let the oracle run BASELINE configs at full geometry (C3:
+ * 2 Mpx, C4: 8 Mpx) in host memory and time; each restates one numpy
+ * expression of the reference.
+ * ------------------------------------------------------------------- */
+
+/* f32 KDE tables of one plane (scene_prior.build_kde :104-111, then the
+ * engine's astype(float32), cascade.py:192): counts = histogram of the N
+ * values of each pixel, table[g] = (sum_s counts[s] * kern[s][g]) / N.
+ * values u8[N][P] (one plane, frame-major), out f32[P][256].  The dot
+ * products run over the nonzero bins in ascending order (zero bins add
+ * +0.0); BLAS may sum the 256 products in another order, which moves the
+ * binary64 result by at most an ulp and, after rounding to float32,
+ * leaves the table identical (pinned on the reference's goldens,
+ * tests/test_oracle.py). */
+int cogo_kde_tables32(int64_t P, int N, const uint8_t *values,
+                      const double *kern, float *out, int threads)
+{
+    int nt = oracle_threads(threads);
+    (void)nt;
+    const int64_t B = 64;
+    int64_t nb = (P + B - 1) / B;
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nt) if (nt > 1)
+    for (int64_t b = 0; b < nb; b++) {
+        int64_t p0 = b * B, p1 = p0 + B < P ? p0 + B : P;
+        uint16_t hist[64][256];
+        memset(hist, 0, sizeof(hist));
+        for (int i = 0; i < N; i++) {
+            const uint8_t *row = values + (int64_t)i * P;
+            for (int64_t p = p0; p < p1; p++) hist[p - p0][row[p]]++;
+        }
+        for (int64_t p = p0; p < p1; p++) {
+            const uint16_t *h = hist[p - p0];
+            int s_idx[256], ns = 0;
+            for (int s = 0; s < 256; s++)
+                if (h[s]) s_idx[ns++] = s;
+            float *o = out + p * 256;
+            for (int g = 0; g < 256; g++) {
+                double acc = 0.0;
+                for (int j = 0; j < ns; j++) {
+                    int s = s_idx[j];
+                    acc = acc + (double)h[s] * kern[s * 256 + g];
+                }
+                o[g] = (float)(acc / (double)N);
+            }
+        }
+    }
+    return 0;
+}
+
+/* k-means assignment step (grouping.py:116-118):
+ * dist = ((f[:, None, :] - c[None]) ** 2).sum(axis=2); argmin(axis=1)
+ * (first minimum on ties).  f f64[n][2], c f64[k][2]; writes label i64[n];
+ * returns 1 if any label changed. */
+int cogo_kmeans_assign(int64_t n, const double *f, int k, const double *c,
+                       int64_t *label, int threads)
+{
+    int nt = oracle_threads(threads);
+    (void)nt;
+    int changed = 0;
+#pragma omp parallel for schedule(static) num_threads(nt) if (nt > 1) \
+    reduction(| : changed)
+    for (int64_t i = 0; i < n; i++) {
+        double best = 0.0;
+        int64_t arg = 0;
+        for (int j = 0; j < k; j++) {
+            double d0 = f[2 * i] - c[2 * j], d1 = f[2 * i + 1] - c[2 * j + 1];
+            double dd = d0 * d0 + d1 * d1;
+            if (j == 0 || dd < best || (isnan(dd) && !isnan(best))) {
+                best = dd;
+                arg = j;
+            }
+        }
+        if (label[i] != arg) changed = 1;
+        label[i] = arg;
+    }
+    return changed;
+}
+
+/* Group sums of one plane for _update_groups (cascade.py:320-344): over the
+ * pixels with kind == GROUP, in pixel order like np.bincount: cnt[g],
+ * vsum[g] (sum of v as f64) and csum[g] (sum of conf, sequential). */
+int cogo_group_sums(int64_t P, const uint8_t *kind, const uint8_t *vals,
+                    const double *conf, const int64_t *group_id, int64_t G,
+                    int64_t *cnt, double *vsum, double *csum)
+{
+    for (int64_t g = 0; g < G; g++) {
+        cnt[g] = 0;
+        vsum[g] = 0.0;
+        csum[g] = 0.0;
+    }
+    for (int64_t p = 0; p < P; p++) {
+        if (kind[p] != L_GROUP) continue;
+        int64_t g = group_id[p];
+        cnt[g] += 1;
+        vsum[g] = vsum[g] + (double)vals[p];
+        csum[g] = csum[g] + conf[p];
     }
     return 0;
 }

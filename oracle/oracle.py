@@ -68,6 +68,9 @@ def lib():
             + [_P] * 4 + [_I])
         L.cogo_resolve_copies.argtypes = [_I64, _P, _P, _P, _I64, _I64]
         L.cogo_sort_pixels.argtypes = [_I64, _P, _I, _P, _P, _P, _P, _P]
+        L.cogo_kde_tables32.argtypes = [_I64, _I, _P, _P, _P, _I]
+        L.cogo_kmeans_assign.argtypes = [_I64, _P, _I, _P, _P, _I]
+        L.cogo_group_sums.argtypes = [_I64, _P, _P, _P, _P, _I64, _P, _P, _P]
         _lib = L
     return _lib
 
@@ -92,21 +95,49 @@ def kernel_matrix(bandwidth: float) -> np.ndarray:
     return m / m.sum(axis=1, keepdims=True)
 
 
-def kde(values: np.ndarray, bandwidth: float):
+def kde(values: np.ndarray, bandwidth: float, chunk: int = 1 << 16):
     """values (N, d, P) uint8 -> (counts (d,P,256) int64, tables (d,P,256) f64).
 
     counts are the bit-exact histogram; tables = counts @ W / N as in
-    scene_prior.py:104-111 (BLAS order)."""
+    scene_prior.py:104-111 (BLAS order; the product is formed over pixel
+    chunks, which leaves every row's dot products unchanged)."""
     n, d, p = values.shape
-    kern = kernel_matrix(bandwidth)
     counts = np.empty((d, p, 256), dtype=np.int64)
     tables = np.empty((d, p, 256), dtype=np.float64)
-    base = np.arange(p, dtype=np.int64) * 256
-    for c in range(d):
-        flat = (base[None, :] + values[:, c].astype(np.int64)).ravel()
-        counts[c] = np.bincount(flat, minlength=p * 256).reshape(p, 256)
-        tables[c] = (counts[c].astype(np.float64) @ kern) / n
+    for c, c0, c1, cnt, tab in _kde_chunks(values, bandwidth, chunk):
+        counts[c, c0:c1] = cnt
+        tables[c, c0:c1] = tab
     return counts, tables
+
+
+def kde_tables32(values: np.ndarray, bandwidth: float) -> np.ndarray:
+    """The f32 tables the engine keeps (cascade.py:192) for (N, d, P) uint8
+    values, without materialising the int64 counts or the f64 table (a 4K
+    prior): cogo_kde_tables32, the same counts @ W / N per pixel with the
+    dot products over the nonzero bins (identical after rounding to f32,
+    tests/test_oracle.py)."""
+    n, d, p = values.shape
+    kern = np.ascontiguousarray(kernel_matrix(bandwidth))
+    out = np.empty((d, p, 256), dtype=np.float32)
+    for c in range(d):
+        plane = np.ascontiguousarray(values[:, c])
+        rc = lib().cogo_kde_tables32(p, n, _ptr(plane), _ptr(kern),
+                                     _ptr(out[c]), default_threads())
+        assert rc == 0
+    return out
+
+
+def _kde_chunks(values, bandwidth, chunk):
+    n, d, p = values.shape
+    kern = kernel_matrix(bandwidth)
+    for c in range(d):
+        for c0 in range(0, p, chunk):
+            c1 = min(p, c0 + chunk)
+            m = c1 - c0
+            base = np.arange(m, dtype=np.int64) * 256
+            flat = (base[None, :] + values[:, c, c0:c1].astype(np.int64)).ravel()
+            cnt = np.bincount(flat, minlength=m * 256).reshape(m, 256)
+            yield c, c0, c1, cnt, (cnt.astype(np.float64) @ kern) / n
 
 
 def residue(values: np.ndarray, t1: float, t2: float):
@@ -215,12 +246,16 @@ def kmeans(features, k, seed, max_iter=100):
         centers[j] = features[int(np.argmax(d2))]
         d2 = np.minimum(d2, ((features - centers[j]) ** 2).sum(axis=1))
     assign = np.full(n, -1, dtype=np.int64)
+    feats = np.ascontiguousarray(features, dtype=np.float64)
+    nxt = assign.copy()
     for _ in range(max_iter):
-        dist = ((features[:, None, :] - centers[None, :, :]) ** 2).sum(axis=2)
-        nxt = np.argmin(dist, axis=1)
-        if np.array_equal(nxt, assign):
+        # dist = ((f[:, None] - c[None]) ** 2).sum(axis=2); argmin (C loop)
+        changed = lib().cogo_kmeans_assign(n, _ptr(feats), k,
+                                           _ptr(np.ascontiguousarray(centers)),
+                                           _ptr(nxt), default_threads())
+        if not changed:
             break
-        assign = nxt
+        assign = nxt.copy()
         for j in range(k):
             mem = features[assign == j]
             if mem.shape[0]:
@@ -242,6 +277,43 @@ def threshold_clusters(assign, features, c):
     return member
 
 
+# pools above this many f64 bytes are not materialised (a 4K group holds
+# ~1e9 training intensities); the engine uses the same bound
+# (paper_1705_09339_b200/grouping.py _POOL_EXACT_BYTES)
+POOL_EXACT_BYTES = 1 << 31
+
+
+def pooled_stats(values, sel, floor):
+    """grouping.py:189-192: mean / floored variance of every training
+    intensity of the members, per channel.  Pools within POOL_EXACT_BYTES
+    use the reference's numpy expression verbatim; bigger ones use exact
+    integer sums (the mean is then identical -- numpy's float sum of
+    integers is exact -- and the variance is the exact rational
+    (M*sum x^2 - (sum x)^2) / M^2 correctly rounded, within a few ulp of
+    numpy's two-pass float evaluation)."""
+    n, d, _ = values.shape
+    m = int(sel.sum())
+    if n * d * m * 8 <= POOL_EXACT_BYTES:
+        pooled = values[:, :, sel].astype(np.float64)
+        return (pooled.mean(axis=(0, 2)),
+                np.maximum(pooled.var(axis=(0, 2), ddof=0), floor))
+    idx = np.where(sel)[0]
+    s1 = [0] * d
+    s2 = [0] * d
+    step = max(1, (1 << 26) // n)
+    for a in range(0, m, step):
+        blk = values[:, :, idx[a:a + step]].astype(np.int64)
+        for c in range(d):
+            x = blk[:, c]
+            s1[c] += int(x.sum())
+            s2[c] += int((x * x).sum())
+    cnt = n * m
+    mean = np.array([s1[c] / cnt for c in range(d)])
+    var = np.array([max((cnt * s2[c] - s1[c] * s1[c]) / (cnt * cnt), floor)
+                    for c in range(d)])
+    return mean, var
+
+
 def group_params(member, values, w_final, cfg):
     """grouping.py:164-195: dense renumbering + pooled per-channel mode."""
     n, d, p = values.shape
@@ -256,9 +328,7 @@ def group_params(member, values, w_final, cfg):
         sel = member == j
         gid[sel] = gi
         mem[gi] = sel.sum()
-        pooled = values[:, :, sel].astype(np.float64)
-        mu[gi] = pooled.mean(axis=(0, 2))
-        var[gi] = np.maximum(pooled.var(axis=(0, 2), ddof=0), cfg.variance_floor)
+        mu[gi], var[gi] = pooled_stats(values, sel, cfg.variance_floor)
         wgt[gi] = w_final[sel].mean()
     return gid, mu, var, wgt, mem
 
@@ -297,8 +367,9 @@ class OracleEngine:
         self.wa = np.zeros(p)
         self.wb = np.zeros(p)
         self.wc = np.zeros(p)
+        # the f32 prior (cascade.py:192); every use promotes an entry to
+        # binary64 exactly as the reference's _tables64 = f64(f32 table)
         self.tables = np.zeros((depth, p, 256), dtype=np.float32)
-        self.tables64 = np.zeros((depth, p, 256))
         self.peaks = np.ones((depth, p))
         self.group_id = np.full(p, -1, dtype=np.int64)
         self.group_mu = np.zeros((depth, 0))
@@ -328,8 +399,7 @@ class OracleEngine:
 
     def finalize_tables(self):
         """cascade.py:213-216."""
-        self.tables64 = self.tables.astype(np.float64)
-        self.peaks = self.tables64.max(axis=2)
+        self.peaks = self.tables.max(axis=2).astype(np.float64)
         self.peaks[self.peaks <= 0.0] = 1.0
 
     def seed_level_order(self):
@@ -340,7 +410,8 @@ class OracleEngine:
         for c in range(self.depth):
             mval = np.clip(np.rint(self.mu[c]), 0, 255).astype(np.int64)
             live = np.arange(k)[None, :] < self.count[c][:, None]
-            mass = np.where(live, self.tables64[c][ar[:, None], mval], -np.inf)
+            mass = np.where(live, self.tables[c][ar[:, None], mval].astype(np.float64),
+                            -np.inf)
             tie = np.where(live, self.w[c] / np.sqrt(self.var[c]), -np.inf)
             order = np.lexsort((-tie, -mass), axis=1)
             self.mode_ref[c, :, 0] = order[:, 0]
@@ -392,7 +463,7 @@ class OracleEngine:
                 _ptr(self.streak[c]), _ptr(self.last_active[c]),
                 _ptr(self.clock[c]), _ptr(self.waking[c]),
                 _ptr(self.on_lattice), _ptr(self.group_id), _ptr(gmu),
-                _ptr(gvar), _ptr(self.tables64[c]), _ptr(self.peaks[c]),
+                _ptr(gvar), _ptr(self.tables[c]), _ptr(self.peaks[c]),
                 _ptr(self.wa), _ptr(self.wb), _ptr(self.wc),
                 cfg.learning_rate, cfg.match_lambda, cfg.background_threshold,
                 cfg.variance_floor, cfg.initial_variance, cfg.chp_epsilon,
@@ -428,16 +499,21 @@ class OracleEngine:
     def update_groups(self, c, vals, kinds, confs):
         """cascade.py:320-344 (sequential bincount sums)."""
         cfg = self.cfg
-        sel = kinds == LEVEL_GROUP
-        if not sel.any():
-            return
         g = self.group_w.shape[0]
-        gids = self.group_id[sel]
-        cnt = np.bincount(gids, minlength=g)
+        cnt = np.empty(g, dtype=np.int64)
+        vs = np.empty(g)
+        cs = np.empty(g)
+        # np.bincount over the GROUP pixels in pixel order (C loop)
+        lib().cogo_group_sums(self.n_pix, _ptr(np.ascontiguousarray(kinds)),
+                              _ptr(np.ascontiguousarray(vals)),
+                              _ptr(np.ascontiguousarray(confs)),
+                              _ptr(self.group_id), g, _ptr(cnt), _ptr(vs),
+                              _ptr(cs))
         act = cnt > 0
-        vbar = np.bincount(gids, weights=vals[sel].astype(np.float64),
-                           minlength=g)[act] / cnt[act]
-        cbar = np.bincount(gids, weights=confs[sel], minlength=g)[act] / cnt[act]
+        if not act.any():
+            return
+        vbar = vs[act] / cnt[act]
+        cbar = cs[act] / cnt[act]
         rho = cfg.learning_rate * np.maximum(1.0 - cbar, cfg.rate_floor)
         m = (1.0 - rho) * self.group_mu[c, act] + rho * vbar
         dlt = vbar - m
@@ -492,7 +568,9 @@ class OracleEngine:
                               (LEVEL_MEAN, self.mu[c][ar, self.mode_ref[c, :, 0]]),
                               (LEVEL_MEANVAR, self.mu[c][ar, self.mode_ref[c, :, 1]])):
                 lv = np.clip(np.rint(lmu), 0, 255).astype(np.int64)
-                pm = np.broadcast_to(self.tables64[c][ar, lv][:, None], codes.shape)
+                pm = np.broadcast_to(
+                    self.tables[c][ar, lv].astype(np.float64)[:, None],
+                    codes.shape)
                 sel = codes == code
                 mass[sel] = pm[sel]
             order = np.lexsort((-mass, -hv), axis=1)
@@ -503,7 +581,7 @@ class OracleEngine:
         return {n: getattr(self, n) for n in self.STATE}
 
 
-def build_engine(cfg, tables64, classes, gid, gmu, gvar, gw, gmem, grids,
+def build_engine(cfg, tables32, classes, gid, gmu, gvar, gw, gmem, grids,
                  height, width, last_values) -> OracleEngine:
     """cascade.py:166-211 (CascadeEngine.build)."""
     d = len(grids)
@@ -513,7 +591,7 @@ def build_engine(cfg, tables64, classes, gid, gmu, gvar, gw, gmem, grids,
     eng.wa = np.ascontiguousarray(wts[:, 0])
     eng.wb = np.ascontiguousarray(wts[:, 1])
     eng.wc = np.ascontiguousarray(wts[:, 2])
-    eng.tables = tables64.astype(np.float32)
+    eng.tables = tables32
     eng.group_id = gid.copy()
     eng.group_mu = np.ascontiguousarray(gmu.T.copy())
     eng.group_var = np.ascontiguousarray(gvar.T.copy())
@@ -531,7 +609,7 @@ def train(values: np.ndarray, cfg) -> OracleEngine:
     """training.train_engine over (N, d, H, W) uint8 training frames."""
     n, d, h, wdt = values.shape
     flat = np.ascontiguousarray(values.reshape(n, d, h * wdt))
-    _, tables = kde(flat, cfg.kde_bandwidth)
+    tables = kde_tables32(flat, cfg.kde_bandwidth)
     _, occ = residue(flat, cfg.residue_t1, cfg.residue_t2)
     classes = classify(occ, cfg.peaky_threshold)
     grids, vs, ws = warmup(flat, cfg)

@@ -87,12 +87,16 @@ class Params(ctypes.Structure):
         (n, ctypes.c_int32) for n in (
             "saturation_frames", "sleep_frames", "sampling_on", "grouping_on",
             "rate_scaling_on", "chp_on", "literal_conf", "compat",
-            "exact_group_sums", "pad_")]
+            "exact_group_sums", "variant")]
+
+
+# cog_params.variant: which step kernel (a parity knob; 0 = automatic)
+VARIANTS = {"auto": 0, "general": 1, "lean": 2}
 
 
 class State(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
-        "mu", "var", "w", "meta", "dyn", "streak", "hits", "table", "peak",
+        "mix", "meta", "dyn", "streak", "hits", "table", "peak", "tabq",
         "cls", "gid", "g_mu", "g_var", "g_members", "accum", "sync",
         "deepq", "deeprho")]
 
@@ -106,8 +110,9 @@ class RefState(ctypes.Structure):
 _P = ctypes.c_void_p
 _SIGS = {
     "cog_accum_words": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
-    "cog_table_floats": (ctypes.c_int64, [_P]),
-    "cog_table_pack": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, _P]),
+    "cog_mix_elems": (ctypes.c_int64, [ctypes.c_int32]),
+    "cog_tabq_elems": (ctypes.c_int64, [_P]),
+    "cog_tabq_build": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "cog_deepq_slots": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int64]),
     "cog_prior_build": (ctypes.c_int, [
         _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, _P, _P,
@@ -137,7 +142,6 @@ _SIGS = {
     "cog_event_sync": (ctypes.c_int, [_P]),
     "cog_event_query": (ctypes.c_int, [_P]),
     "cog_version": (ctypes.c_char_p, []),
-    "cog_debug_prof": (ctypes.c_int, [_P, ctypes.c_int]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -192,21 +192,26 @@ class DeviceState:
 
         def z(*shape, dtype):
             return torch.zeros(shape, dtype=dtype, device=dev)
-        self.mu = z(S, d, K, P, dtype=self.tdtype)
-        self.var = z(S, d, K, P, dtype=self.tdtype)
-        self.w = z(S, d, K, P, dtype=self.tdtype)
+        # mixture records (S, d, P, R): (mu_k, var_k) at [2k, 2k+1], w_k at
+        # [2 * KB + k] (include/cog_b200.h); mu / var / w are views
+        self.kb = 3 if K <= 3 else (5 if K <= 5 else 8)
+        self.rec = int(_lib.load().cog_mix_elems(K))
+        self.mix = z(S, d, P, self.rec, dtype=self.tdtype)
         self.meta = z(S, d, P, dtype=torch.int16)
         self.dyn = z(S, d, P, dtype=torch.int32)
         self.streak = z(S, d, P, dtype=torch.int32)
         self.hits = z(S, d, 5, P, dtype=torch.int32)
-        # prior tables in the tile-major layout of the step kernels
-        # (cog_table_pack converts from / to the reference [d][P][256])
-        self.tab_floats = int(_lib.load().cog_table_floats(
-            _lib.ref(self._geom(1))))
-        if self.tab_floats < 0:
-            raise DataError("unsupported engine geometry")
-        self.table = z(S, self.tab_floats, dtype=torch.float32)
+        # the prior in the reference layout (exact values), and for float32
+        # engines its u16 tile-major hot copy (cog_tabq_build)
+        self.table = z(S, d, P, 256, dtype=torch.float32)
         self.peak = torch.ones((S, d, P), dtype=torch.float32, device=dev)
+        if self.f64:
+            self.tabq = None
+        else:
+            n = int(_lib.load().cog_tabq_elems(_lib.ref(self._geom(1))))
+            if n < 0:
+                raise DataError("unsupported engine geometry")
+            self.tabq = z(S, n, dtype=torch.int16)
         self.cls = z(S, P, dtype=torch.uint8)
         self.gid = torch.full((S, P), -1, dtype=torch.int16, device=dev)
         self.g_mu = z(S, d, G1, dtype=torch.float64)
@@ -230,44 +235,62 @@ class DeviceState:
         g.streams, g.state_f64, g.row0 = streams, int(self.f64), self.row0
         return g
 
+    # mixture views (S, d, K, P) of the records
+    @property
+    def mu(self) -> torch.Tensor:
+        return self.mix[..., 0:2 * self.k:2].permute(0, 1, 3, 2)
+
+    @property
+    def var(self) -> torch.Tensor:
+        return self.mix[..., 1:2 * self.k:2].permute(0, 1, 3, 2)
+
+    @property
+    def w(self) -> torch.Tensor:
+        return self.mix[..., 2 * self.kb:2 * self.kb + self.k].permute(0, 1, 3, 2)
+
     def table_to_ref(self, s: int) -> torch.Tensor:
         """Stream s's prior table in the reference layout (d, P, 256)."""
-        out = torch.empty((self.depth, self.P, 256), dtype=torch.float32,
-                          device=self.device)
-        rc = _lib.load().cog_table_pack(
-            _lib.ref(self._geom(1)), out.data_ptr(), self.table[s].data_ptr(),
-            0, torch.cuda.current_stream(self.device).cuda_stream)
-        _lib.check(rc, "cog_table_pack")
-        return out
+        return self.table[s]
 
     def table_from_ref(self, s: int, tables: torch.Tensor) -> None:
-        """Pack a (d, P, 256) f32 device table into stream s."""
-        tables = tables.to(self.device, torch.float32).contiguous()
+        """Install a (d, P, 256) f32 table into stream s (its peak must
+        already be set) and rebuild the hot copy."""
+        tables = tables.to(self.device, torch.float32)
         if tuple(tables.shape) != (self.depth, self.P, 256):
             raise DataError(f"table shape {tuple(tables.shape)} != "
                             f"{(self.depth, self.P, 256)}")
-        rc = _lib.load().cog_table_pack(
-            _lib.ref(self._geom(1)), tables.data_ptr(),
-            self.table[s].data_ptr(), 1,
+        if tables.data_ptr() != self.table[s].data_ptr():
+            self.table[s].copy_(tables)
+        self.build_hot_table(s)
+
+    def build_hot_table(self, s: int) -> None:
+        """u16 tile-major phat of stream s from its table and peak."""
+        if self.tabq is None:
+            return
+        rc = _lib.load().cog_tabq_build(
+            _lib.ref(self._geom(1)), self.table[s].data_ptr(),
+            self.peak[s].data_ptr(), self.tabq[s].data_ptr(),
             torch.cuda.current_stream(self.device).cuda_stream)
-        _lib.check(rc, "cog_table_pack")
+        _lib.check(rc, "cog_tabq_build")
+
+    _BUFS = ("mix", "meta", "dyn", "streak", "hits", "table", "peak", "tabq",
+             "cls", "gid", "g_mu", "g_var", "g_members", "accum", "sync",
+             "deepq", "deeprho")
 
     def _refresh(self) -> None:
         self.geom = self._geom(self.streams)
         st = _lib.State()
-        for name in ("mu", "var", "w", "meta", "dyn", "streak", "hits",
-                     "table", "peak", "cls", "gid", "g_mu", "g_var",
-                     "g_members", "accum", "sync", "deepq", "deeprho"):
-            setattr(st, name, getattr(self, name).data_ptr())
+        for name in self._BUFS:
+            t = getattr(self, name)
+            setattr(st, name, t.data_ptr() if t is not None else None)
         self.cstate = st
 
     def stream_view(self, s: int) -> "_lib.State":
         """C struct pointing at stream s only (for export/import)."""
         st = _lib.State()
-        for name in ("mu", "var", "w", "meta", "dyn", "streak", "hits",
-                     "table", "peak", "cls", "gid", "g_mu", "g_var",
-                     "g_members", "accum", "sync", "deepq", "deeprho"):
-            setattr(st, name, getattr(self, name)[s].data_ptr())
+        for name in self._BUFS:
+            t = getattr(self, name)
+            setattr(st, name, t[s].data_ptr() if t is not None else None)
         return st
 
     def single_geom(self) -> "_lib.Geom":
@@ -436,6 +459,9 @@ class CascadeEngine:
         # reference's sequential pixel order (single thread, small frames);
         # the production path sums them exactly in fixed point instead
         self.exact_group_sums = False
+        # parity switch: which step kernel runs ("auto", "general", "lean");
+        # an engine attribute, never read from the environment
+        self.kernel_variant = "auto"
         yy, xx = np.divmod(np.arange(self.n_pix), width)
         s = config.stride
         self.on_lattice = (((yy + row0) % s == 0) & (xx % s == 0)).astype(np.uint8)
@@ -456,10 +482,11 @@ class CascadeEngine:
         """The C params struct, rebuilt only when an input changes (the
         per-frame launch path must stay cheap on the host)."""
         key = (id(self.config), self._wtab.tobytes(),
-               bool(self.exact_group_sums))
+               bool(self.exact_group_sums), self.kernel_variant)
         if getattr(self, "_pkey", None) != key:
             q = params_from_config(self.config, self._wtab)
             q.exact_group_sums = int(self.exact_group_sums)
+            q.variant = _lib.VARIANTS[self.kernel_variant]
             self._pcache, self._pkey = q, key
         return self._pcache
 

@@ -73,6 +73,19 @@ __device__ __forceinline__ uint32_t pack_dyn(int chp, int label, int waking,
 }
 
 // ----------------------------------------------------------------------------
+// Mixture record of one plane-pixel in HBM (cog_b200.h): KB = the K bucket
+// of the kernel instantiation (k_max <= KB), R elements of the state type:
+// (mu_k, var_k) at [2k, 2k+1], w_k at [2*KB + k], the rest padding.  One
+// record is 64 B (KB <= 5) or 128 B of float32: a pixel's whole mixture is
+// one aligned DRAM burst, and (mu, var) of one mode one 8-byte load.
+// ----------------------------------------------------------------------------
+__host__ __device__ constexpr int kbucket(int K) {
+  return K <= 3 ? 3 : (K <= 5 ? 5 : 8);
+}
+__host__ __device__ constexpr int rec_elems(int KB) { return KB <= 5 ? 16 : 32; }
+__host__ __device__ constexpr int rec_w(int KB) { return 2 * KB; }
+
+// ----------------------------------------------------------------------------
 // Register-resident mixture of one plane-pixel, binary64.
 // ----------------------------------------------------------------------------
 template <int KMAX>
@@ -237,6 +250,72 @@ __device__ __forceinline__ double ldrw(const T* p) {
 }
 __device__ __forceinline__ void st(float* p, double v) { *p = (float)v; }
 __device__ __forceinline__ void st(double* p, double v) { *p = v; }
+
+// whole record <-> registers with 16-byte vector accesses (R is a multiple
+// of 4 floats / 2 doubles; records are 64-B aligned)
+template <int R>
+__device__ __forceinline__ void rec_load(const float* rec, float (&e)[R]) {
+#pragma unroll
+  for (int i = 0; i < R / 4; ++i) {
+    const float4 v = reinterpret_cast<const float4*>(rec)[i];
+    e[4 * i] = v.x;
+    e[4 * i + 1] = v.y;
+    e[4 * i + 2] = v.z;
+    e[4 * i + 3] = v.w;
+  }
+}
+template <int R>
+__device__ __forceinline__ void rec_load(const double* rec, double (&e)[R]) {
+#pragma unroll
+  for (int i = 0; i < R / 2; ++i) {
+    const double2 v = reinterpret_cast<const double2*>(rec)[i];
+    e[2 * i] = v.x;
+    e[2 * i + 1] = v.y;
+  }
+}
+template <int R>
+__device__ __forceinline__ void rec_store(float* rec, const float (&e)[R]) {
+#pragma unroll
+  for (int i = 0; i < R / 4; ++i)
+    reinterpret_cast<float4*>(rec)[i] =
+        make_float4(e[4 * i], e[4 * i + 1], e[4 * i + 2], e[4 * i + 3]);
+}
+template <int R>
+__device__ __forceinline__ void rec_store(double* rec, const double (&e)[R]) {
+#pragma unroll
+  for (int i = 0; i < R / 2; ++i)
+    reinterpret_cast<double2*>(rec)[i] = make_double2(e[2 * i], e[2 * i + 1]);
+}
+
+// record elements <-> binary64 mixture (live modes only; dead slots and
+// padding keep their stored values)
+template <int KMAX, typename T>
+__device__ __forceinline__ void rec_to_mix(const T (&e)[rec_elems(KMAX)],
+                                           int n, Mix<KMAX>& x) {
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    x.mu[k] = 0.0;
+    x.var[k] = 1.0;
+    x.w[k] = 0.0;
+    if (k < n) {
+      x.mu[k] = (double)e[2 * k];
+      x.var[k] = (double)e[2 * k + 1];
+      x.w[k] = (double)e[rec_w(KMAX) + k];
+    }
+  }
+}
+template <int KMAX, typename T>
+__device__ __forceinline__ void mix_to_rec(const Mix<KMAX>& x, int n,
+                                           T (&e)[rec_elems(KMAX)]) {
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k < n) {
+      e[2 * k] = (T)x.mu[k];
+      e[2 * k + 1] = (T)x.var[k];
+      e[rec_w(KMAX) + k] = (T)x.w[k];
+    }
+  }
+}
 
 // warp-wide sums of unsigned values (REDUX on sm_80+)
 __device__ __forceinline__ unsigned warp_sum_u32(unsigned v) {

@@ -7,28 +7,43 @@
 // reference's planes are independent, cascade.py:281) so a thread holds one
 // plane's state at a time.  The union mask is written per tile; labels that
 // arrive with the deep kernel (GMM fall-throughs) are OR-ed in there.
-// (Measured alternatives: one plane per warp with the
-// mask formed in a union pass, and 4 pixels per lane with 16-B accesses --
-// both slower on B200.)
+//
+// Loads per plane-pixel, in two dependent rounds:
+//   round 1 (pixel index): frame byte, dyn, meta, streak -- for all planes
+//            of the tile up front;
+//   round 2 (needs v and meta): the hot prior phat(v) from the u16
+//            tile-major table, and -- only when the cascade can reach a
+//            mode level or the confidence reads a mode (the group test is
+//            settled from shared memory first; ~75 % of plane-pixels stop
+//            at the group level) -- the (mu, var) pairs of the two
+//            referenced modes from the pixel's 64-B mixture record, one
+//            8-byte load each, same DRAM burst.
 // The per-plane-pixel work is split by frequency:
 //   * fast path (the common case: evaluated pixel, sampling clock idle, not
-//     compat, no decision within the filter margin): the cascade written
-//     for fp32 with float constants precomputed on the host (FastConst:
-//     no per-use double->float conversions), integer change test, one
-//     level walk.  It makes exactly the reference's decisions: every fp32
-//     comparison whose operands are within 1e-5 relative bails out;
-//   * slow path: the general hot_px (binary64 fallbacks, SKIP/COPY gating,
-//     compat), called out of line for the rare plane-pixels that need it.
+//     compat, no decision within the filter margins): the cascade in fp32
+//     with float constants precomputed on the host (FastConst), integer
+//     change test, one level walk.  It makes exactly the reference's
+//     decisions: an fp32 comparison whose operands lie within its margin
+//     (the u16 prior's quantisation, 7.7e-6, plus 1e-5 relative) bails out;
+//   * slow path: the general hot_px (binary64 fallbacks from the exact f32
+//     table, SKIP/COPY gating, compat) for the rare plane-pixels that need
+//     it; its exact loads (table entry, peak, modes) are issued only then.
 //   * group partials: a warp-tile is nearly always group-homogeneous, so the
 //     partials are one set of warp reductions added by lane 0 into the
 //     warp's private shared slice (no atomics); mixed tiles loop.
 
 constexpr int FQ_CAP = 64;  // per-warp worklist buffer (one global atomic per flush)
 
+// u16 hot prior: phat = q / 65535 with q = round(phat * 65535), so
+// |phat - q / 65535| <= 0.5 / 65535 (+ the fp32 product's rounding)
+constexpr float PH_Q = 1.0f / 65535.0f;
+constexpr float PH_QERR = 7.7e-6f;
+
 struct FastConst {
-  float lam, t_bg_unused, pf, ct, pf_hi, pf_lo;
+  float lam, pf, ct, pf_margin;
   float w[9];
   float wbc_inv[3];  // 1 / (wb + wc) per class, 0 if wb + wc <= 0
+  float ct_margin[3];  // |conf - ct| below this -> exact path, per class
   int eps_i;         // changed  <=>  |v - chp| > eps_i
   int sat;           // saturation_frames (clamped to int)
 };
@@ -38,10 +53,12 @@ FastConst make_fast_const(const cog_params& q) {
   k.lam = (float)q.match_lambda;
   k.pf = (float)q.prior_floor;
   k.ct = (float)q.confidence_threshold;
+  k.pf_margin = PH_QERR + FILTER_MARGIN * fabsf(k.pf);
   for (int i = 0; i < 9; ++i) k.w[i] = (float)q.weights[i];
   for (int c = 0; c < 3; ++c) {
     const double dd = q.weights[3 * c + 1] + q.weights[3 * c + 2];
     k.wbc_inv[c] = dd > 0.0 ? (float)(1.0 / dd) : 0.0f;
+    k.ct_margin[c] = FILTER_MARGIN + fabsf(k.w[3 * c]) * PH_QERR;
   }
   // |v - chp| is an integer: d > eps  <=>  d > floor(eps)  (eps >= 0)
   const double e = q.chp_epsilon;
@@ -50,20 +67,15 @@ FastConst make_fast_const(const cog_params& q) {
   return k;
 }
 
-// out-of-line general path for the rare plane-pixels (returns by value:
-// taking the address of the caller's HotOut would pin it to local memory)
-#ifdef COG_SLOW_CALL
-#define COG_SLOW_ATTR __noinline__
-#else
-#define COG_SLOW_ATTR __forceinline__  // measured faster than a call
-#endif
+// general path for the rare plane-pixels (returns by value: taking the
+// address of the caller's HotOut would pin it to local memory)
 template <typename T>
-__device__ COG_SLOW_ATTR HotOut hot_px_slow(const StepArgs* __restrict__ a,
-                                           int s, int c, uint32_t p,
-                                           Pre<T> pre, bool on_lat,
-                                           const double* s_bt, int cls,
-                                           bool member, double gmu,
-                                           double gthr) {
+__device__ __forceinline__ HotOut hot_px_slow(const StepArgs* __restrict__ a,
+                                              int s, int c, uint32_t p,
+                                              Pre<T> pre, bool on_lat,
+                                              const double* s_bt, int cls,
+                                              bool member, double gmu,
+                                              double gthr) {
   const Flags f{a->q.sampling_on != 0, a->q.grouping_on != 0,
                 a->q.rate_scaling_on != 0, a->q.chp_on != 0,
                 a->q.literal_conf != 0, a->q.compat != 0};
@@ -87,7 +99,7 @@ __device__ COG_SLOW_ATTR HotOut hot_px_slow(const StepArgs* __restrict__ a,
 
 // single-instruction MUFU approximations (rel. error ~1 ulp): every value
 // they feed is either continuous (within the fp32 tolerance) or a decision
-// protected by the 1e-5 filter margins; operands are normal, positive floats
+// protected by the filter margins; operands are normal, positive floats
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -110,6 +122,22 @@ __device__ __forceinline__ int fmatch(float vf, float mu, float thr) {
   return -1;
 }
 
+// exact operands of the binary64 path: f32 table entry at v, peak, and the
+// two referenced modes (from the record)
+__device__ __forceinline__ void load_exact(const float* table,
+                                           const float* peak, const float* rec,
+                                           uint32_t o, Pre<float>& x) {
+  x.tv = __ldcg(table + (size_t)o * 256 + x.vb);
+  x.peak = __ldg(peak + o);
+  const uint32_t r0 = (x.meta >> 10) & 7u, r1 = x.meta >> 13;
+  const float2 m0 = *reinterpret_cast<const float2*>(rec + 2 * r0);
+  const float2 m1 = *reinterpret_cast<const float2*>(rec + 2 * r1);
+  x.mu0 = m0.x;
+  x.var0 = m0.y;
+  x.mu1 = m1.x;
+  x.var1 = m1.y;
+}
+
 #ifndef COG_FAST_MINB
 #define COG_FAST_MINB 3
 #endif
@@ -119,6 +147,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
     fast_kernel(const __grid_constant__ StepArgs a,
                 const __grid_constant__ FastConst k) {
   using T = float;
+  constexpr int R = rec_elems(KMAX), WO = rec_w(KMAX);
   extern __shared__ double s_mem[];
   const int s = blockIdx.y;
   const int G = a.g.n_groups, K = a.g.k;
@@ -169,14 +198,16 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
   double* qr = s_qr + warp * FQ_CAP;
 
   // 32-bit element indices from the state arrays' own bases (the launcher
-  // guarantees streams * d * max(K, 5) * P < 2^32); the bases stay uniform
+  // guarantees streams * d * max(K, 5) * P and the record elements < 2^32);
+  // the bases stay uniform
   const uint32_t sP = (uint32_t)s * D * P;      // [s][d][P] arrays
   const uint32_t sK = (uint32_t)s * D;          // plane index base
   const uint32_t s1 = (uint32_t)s * P;          // [s][P] arrays
-  T* const mu_s = (T*)a.s.mu;
-  T* const var_s = (T*)a.s.var;
-  T* const w_s = (T*)a.s.w;
+  T* const mix_s = (T*)a.s.mix;
   T* const conf_s = (T*)a.conf;
+  const float* const table_s = a.s.table;
+  const float* const peak_s = a.s.peak;
+  const uint16_t* const tabq_s = a.s.tabq;
   uint32_t* sync = a.s.sync + (size_t)s * 4;
   const size_t dq_cap = dq_capacity(D, P);
   unsigned long long* dq_code =
@@ -202,8 +233,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
   // shared rows stay in the same DRAM pages and L2 lines) when every warp
   // has many tiles; with few tiles per warp (C2: 2-3) the one-tile
   // difference between warps decides the SM balance, and ranks interleaved
-  // over the CTAs spread the longer warps evenly (C2: 64-65 tiles per SM
-  // instead of 48 or 72; 70.9 -> 69.5 us, while C3/C4 lose 2-3 % with it)
+  // over the CTAs spread the longer warps evenly.
   const int nw = gridDim.x * LEAN_WARPS;
   const bool spread = a.n_tiles / nw < 8;
   int wt = spread ? warp * gridDim.x + blockIdx.x
@@ -243,6 +273,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
     const int cls = valid ? (int)a.s.cls[s1 + p] : 0;
     const bool member = valid && G > 0 && gid != (int)UNGROUPED;
     const float wa = k.w[3 * cls], wb = k.w[3 * cls + 1], wc = k.w[3 * cls + 2];
+    const float ct_m = k.ct_margin[cls];
     const unsigned any_member = __ballot_sync(FULL, member);
     int fg = 0;
 
@@ -254,14 +285,12 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
     auto load1 = [&](int c, Pre<T>& x) {
       x.vb = 0;
       x.dyn = x.meta = x.streak = 0u;
-      x.peak = 1.0f;
       if (valid) {
         const uint32_t o = sP + (uint32_t)c * P + p;
         x.vb = a.frame[o];
         x.dyn = a.s.dyn[o];
         x.meta = a.s.meta[o];
         x.streak = a.s.streak[o];
-        x.peak = __ldg(a.s.peak + o);
       }
     };
     load1(0, n0);
@@ -270,42 +299,59 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
 #pragma unroll 1
     for (int c = 0; c < D; ++c) {
     const uint32_t o = sP + (uint32_t)c * P + p;
-    const uint32_t mb = (sK + c) * K * P + p;  // mode 0 of this plane-pixel
+    T* const rec = mix_s + o * R;  // this plane-pixel's mixture record
     Pre<T> x = n0;
     if (D > 1) n0 = n1;
     if (D > 2) n1 = n2;
     x.tv = 0.0f;
+    x.peak = 1.0f;
     x.mu0 = x.mu1 = 0.0f;
     x.var0 = x.var1 = 1.0f;
+    const int gidx = member ? c * G + gid : 0;
+    const float vf = (float)x.vb;
+    const int chp = x.dyn & 0xFF;
+    const int dv = abs(x.vb - chp);
+    const bool changed = dv > k.eps_i;
+    // rare gating states (sleeping / waking clock) and compat go to the
+    // general path with exact operands
+    bool slow = compat || (sampling && ((x.dyn >> 9 & 1u) || (x.dyn >> 16)));
+    const bool ev = valid && !compat &&
+                    will_evaluate(sampling, x.dyn, x.vb, on_lat,
+                                  a.q.chp_epsilon);
+    const uint32_t meta = x.meta;
+    const uint32_t c0 = (meta >> 4) & 3u, c1 = (meta >> 6) & 3u,
+                   c2 = (meta >> 8) & 3u;
+    uint32_t top = c0;
+    if (top == L_GROUP && !grouping) top = c1;
+    const bool gtop = top == L_GROUP && member;
+    const float gm = member ? s_gmuf[gidx] : 0.0f;
+    const float gt_thr = member ? s_gthrf[gidx] : 1.0f;
+    // the group test from shared memory: does the level walk stop at GROUP
+    // before any mode level?  (only GROUP codes ahead of the first mode
+    // code matter; an undecided test loads the modes and bails later)
+    int ghit = (grouping && member) ? fmatch(vf, gm, gt_thr) : 0;
+    bool need_modes = !gtop;
+    if (!(chp_on && !changed)) {
+      const bool walk_stops = (c0 == L_GROUP && ghit == 1);
+      need_modes |= !walk_stops;
+    }
+    uint16_t q16 = 0;
 
-    // ---- round 2: table entry at v, the MEAN / MEANVAR modes
-    if (valid && !compat &&
-        will_evaluate(sampling, x.dyn, x.vb, on_lat, a.q.chp_epsilon)) {
-#ifdef COG_EXP_NOTABLE
-      x.tv = 0.01f * (float)(o & 7);
-#else
-      // tile-major table: plane (sK + c), this tile, bin v, slot = lane
-      x.tv = __ldcg(a.s.table +
-                    (((size_t)(sK + c) * a.n_tiles + tile) * 256 + x.vb) * 32 +
-                    lane);
-#endif
-      const uint32_t r0 = (x.meta >> 10) & 7u, r1 = x.meta >> 13;
-#ifdef COG_EXP_NOMODES
-      x.mu0 = 100.0f + (float)(p & 3); x.var0 = 16.0f; x.mu1 = x.mu0; x.var1 = x.var0;
-      if (0) {
-#endif
-      x.mu0 = mu_s[mb + r0 * P];
-      x.var0 = var_s[mb + r0 * P];
-      if (r1 != r0) {
-        x.mu1 = mu_s[mb + r1 * P];
-        x.var1 = var_s[mb + r1 * P];
-      } else {
-        x.mu1 = x.mu0;
-        x.var1 = x.var0;
+    // ---- round 2: hot prior at v; the referenced modes if needed
+    if (ev && !slow) {
+      q16 = __ldcg(tabq_s + (((size_t)(sK + c) * a.n_tiles + tile) * 256 +
+                             x.vb) * 32 + lane);
+      if (need_modes) {
+        const uint32_t r0 = (meta >> 10) & 7u, r1 = meta >> 13;
+        const float2 m0 = *reinterpret_cast<const float2*>(rec + 2 * r0);
+        const float2 m1 = *reinterpret_cast<const float2*>(rec + 2 * r1);
+        x.mu0 = m0.x;
+        x.var0 = m0.y;
+        x.mu1 = m1.x;
+        x.var1 = m1.y;
       }
-#ifdef COG_EXP_NOMODES
-      }
-#endif
+    } else if (ev) {
+      load_exact(table_s, peak_s, rec, o, x);
     }
     HotOut ho;
     ho.kind = 0;
@@ -315,37 +361,24 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
     ho.rho = 0.0;
     ho.rsel = 0;
     ho.dyn = 0;
-    const int gidx = member ? c * G + gid : 0;
     if (valid) {
-      const int vb = x.vb;
-      const uint32_t dyn = x.dyn, meta = x.meta;
-      const int chp = dyn & 0xFF;
-      const int dv = abs(vb - chp);
-      const bool changed = dv > k.eps_i;
-      // rare gating states go to the general path
-      bool slow = compat || (sampling && (dyn >> 9 & 1u || dyn >> 16));
+      const uint32_t dyn = x.dyn;
       int active = -1, label = 0;
       float cf = 0.0f;
       double rho = 0.0;
       uint32_t r0 = 0, r1 = 0;
       if (!slow) {
-        const float vf = (float)vb;
-        const uint32_t c0 = (meta >> 4) & 3u, c1 = (meta >> 6) & 3u,
-                       c2 = (meta >> 8) & 3u;
         r0 = (meta >> 10) & 7u;
         r1 = meta >> 13;
-        uint32_t top = c0;
-        if (top == L_GROUP && !grouping) top = c1;
-        const bool gtop = top == L_GROUP && member;
         const bool top1 = top == L_MEANVAR;
-        const float s0 = x.var0 * rsqrt_approx(x.var0),
-                    s1 = x.var1 * rsqrt_approx(x.var1);
-        const float thr0 = k.lam * s0, thr1 = k.lam * s1;
-        const float gm = member ? s_gmuf[gidx] : 0.0f;
-        const float gt_thr = member ? s_gthrf[gidx] : 1.0f;
+        float thr0 = 1.0f, thr1 = 1.0f;
+        if (need_modes) {
+          thr0 = k.lam * (x.var0 * rsqrt_approx(x.var0));
+          thr1 = k.lam * (x.var1 * rsqrt_approx(x.var1));
+        }
         const float mt = gtop ? gm : (top1 ? x.mu1 : x.mu0);
         const float dn = gtop ? gt_thr : (top1 ? thr1 : thr0);
-        const float ph = x.tv * rcp_approx(x.peak);
+        const float ph = (float)q16 * PH_Q;
         const float bt = s_btf[dv];
         float gt = fminf(fabsf(vf - mt) * rcp_approx(dn), 1.0f);
         if (!literal) gt = 1.0f - gt;
@@ -353,8 +386,8 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
           cf = (wb * bt + wc * gt) * k.wbc_inv[cls];
         else
           cf = wa * ph + wb * bt + wc * gt;
-        slow = fabsf(ph - k.pf) <= FILTER_MARGIN * k.pf + 1e-30f ||
-               fabsf(cf - k.ct) <= FILTER_MARGIN;
+        slow = fabsf(ph - k.pf) <= k.pf_margin ||
+               fabsf(cf - k.ct) <= ct_m;
         if (chp_on && !changed) {
           active = L_CHP;
           label = (dyn >> 8) & 1u;
@@ -367,7 +400,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
             int hit;
             uint32_t rr = 0;
             if (code == L_GROUP) {
-              hit = (grouping && member) ? fmatch(vf, gm, gt_thr) : 0;
+              hit = ghit;
             } else if (code == L_MEAN) {
               rr = r0;
               hit = fmatch(vf, x.mu0, thr0);
@@ -383,7 +416,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
               // matched mode must sit inside the background weight prefix
               double acc = 0.0;
               for (uint32_t q = 0; q < rr; ++q)
-                acc = acc + (double)w_s[mb + q * P];
+                acc = acc + (double)rec[WO + q];
               hit = acc <= a.q.background_threshold;
             }
             if (hit) active = (int)code;
@@ -397,6 +430,8 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
             if (relax < a.q.rate_floor) relax = a.q.rate_floor;
             rho = a.q.learning_rate * relax;
           }
+        } else {
+          load_exact(table_s, peak_s, rec, o, x);  // rare: exact operands
         }
       }
       if (slow) {
@@ -406,8 +441,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
       } else {
         // ---- bookkeeping of the fast path (kernels_numba.py:335-359)
         if (active == L_MEAN) {
-          st(mu_s + (mb + r0 * P),
-             (1.0 - rho) * (double)x.mu0 + rho * (double)vb);
+          rec[2 * r0] = (float)((1.0 - rho) * (double)x.mu0 + rho * (double)x.vb);
         } else if (active == L_MEANVAR) {
           ho.deep = DEEP_MEANVAR;
           ho.rsel = (int)r1;
@@ -420,22 +454,18 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
         else
           sk = 0u;
         a.s.streak[o] = sk;
-#ifndef COG_EXP_NORED
         atomicAdd(a.s.hits + (((sK + c) * 5 + (uint32_t)active) * P + p), 1u);
-#endif
         const int clock = (sampling && (long long)sk >= (long long)k.sat)
                               ? a.q.sleep_frames : (int)(dyn >> 16);
         ho.kind = active;
         ho.label = label;
         ho.conf = (double)cf;
         ho.rho = rho;
-        ho.dyn = pack_dyn(vb, label, (dyn >> 9) & 1u, active, clock);
+        ho.dyn = pack_dyn(x.vb, label, (dyn >> 9) & 1u, active, clock);
         if (active != L_GMM) a.s.dyn[o] = ho.dyn;
       }
-#ifndef COG_EXP_NOSTORE
       st(conf_s + o, ho.conf);
       a.kind[o] = (uint8_t)ho.kind;
-#endif
       kc += 1ull << (9 * ho.kind);
     }
     int label = ho.label & 1;
@@ -500,11 +530,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
     fg |= label;
 
     // ---- group partials (exact sums) into the warp's private slice
-#ifdef COG_EXP_NOGROUP
-    if (0) {
-#else
     if (any_member) {
-#endif
       unsigned todo = any_member;
       while (todo) {
         const int leader = __ffs(todo) - 1;
@@ -539,7 +565,6 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_FAST_MINB)
         }
       }
     }
-  
     }  // planes
 
     if (valid) a.mask[s1 + p] = fg ? 255 : 0;

@@ -32,8 +32,7 @@
 #include "cog_device.cuh"
 #include "../../include/cog_b200.h"
 
-#include <cstdio>
-#include <cstdlib>
+#include <cmath>
 #include <mutex>
 
 using namespace cog;
@@ -77,15 +76,17 @@ struct StepArgs {
 };
 
 // ---------------------------------------------------------------------------
-// Prior-table layout.  The step reads ONE entry of a pixel's 256-bin table
-// per frame (at the pixel's value v).  Stored pixel-major (the reference's
-// [P][256]), every lookup of a warp is 32 random 128-B DRAM fetches.  Stored
-// tile-major instead -- per plane [n_tiles][256][SL], the SL slots of a bin
-// being the pixels of one warp tile (stride rows x cw columns, slot =
-// row * cw + col, SL = iters * 32) -- the lanes of a warp that see the same
-// value share one 128-B line (measured on C2: 16.7 lines per warp-plane
-// instead of 32, -57 MB DRAM per frame).  Host views and model files use
-// the reference layout; cog_table_pack converts.
+// Hot prior layout (tabq).  The float32 step reads ONE entry of a pixel's
+// 256-bin prior per frame (at the pixel's value v).  Pixel-major (the
+// reference's [P][256]) every lookup of a warp is a random DRAM line.  The
+// hot copy is tile-major -- per plane [n_tiles][256][SL], the SL slots of a
+// bin being the pixels of one warp tile (stride rows x cw columns, slot =
+// row * cw + col, SL = iters * 32) -- so lanes of a warp that see the same
+// value share a line, and it holds phat = table / peak quantised to u16, so
+// a 128-B line covers two bins (a warp tile's ~17 distinct values touch
+// ~9 lines instead of 17).  The exact f32 table stays in the reference
+// layout for the binary64 paths, the decisions the u16 value cannot settle,
+// and model files.
 // ---------------------------------------------------------------------------
 struct TabGeo {
   uint32_t W, st, cw, tiles_x, SL;
@@ -123,45 +124,6 @@ __device__ __forceinline__ size_t tab_pix(const TabGeo& t, size_t p) {
   return (size_t)(ty * t.tiles_x + tx) * 256 * t.SL + r * t.cw + col;
 }
 
-template <typename T>
-struct MixPtrs {
-  T* mu;
-  T* var;
-  T* w;
-};
-
-// ---------------------------------------------------------------------------
-// mixture load / store (k-th mode of a plane-pixel lives at k*P + p)
-// ---------------------------------------------------------------------------
-template <typename T, int KMAX>
-__device__ __forceinline__ void load_mix(const MixPtrs<T>& m, size_t P,
-                                         size_t p, int n, Mix<KMAX>& x) {
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k) {
-    x.mu[k] = 0.0;
-    x.var[k] = 1.0;
-    x.w[k] = 0.0;
-    if (k < n) {
-      x.mu[k] = ldrw(m.mu + k * P + p);
-      x.var[k] = ldrw(m.var + k * P + p);
-      x.w[k] = ldrw(m.w + k * P + p);
-    }
-  }
-}
-
-template <typename T, int KMAX>
-__device__ __forceinline__ void store_mix(const MixPtrs<T>& m, size_t P,
-                                          size_t p, int n, const Mix<KMAX>& x) {
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k) {
-    if (k < n) {
-      st(m.mu + k * P + p, x.mu[k]);
-      st(m.var + k * P + p, x.var[k]);
-      st(m.w + k * P + p, x.w[k]);
-    }
-  }
-}
-
 __device__ __forceinline__ double clip_rint(double x) {
   double r = rint(x);
   return r < 0.0 ? 0.0 : (r > 255.0 ? 255.0 : r);
@@ -173,17 +135,15 @@ __device__ __forceinline__ double clip_rint(double x) {
 // ---------------------------------------------------------------------------
 template <typename T>
 struct PlaneRef {
-  T* mu;
-  T* var;
-  T* w;
+  T* mix;              // this plane's mixture records, R elements each
   uint16_t* meta;
   uint32_t* dyn;
   uint32_t* streak;
   uint32_t* hits;
-  const float* table;  // this plane's tile-major prior table
+  const float* table;  // this plane's prior, reference layout [P][256]
   const float* peak;
   size_t P;
-  TabGeo tg;
+  int R, KB;           // record length and K bucket (w_k at 2 * KB + k)
 };
 
 template <typename T>
@@ -191,49 +151,46 @@ __device__ __forceinline__ PlaneRef<T> plane_ref(const StepArgs& a, int s,
                                                  int c) {
   const size_t P = (size_t)a.g.height * a.g.width;
   const size_t sc = (size_t)s * a.g.depth + c;
-  const size_t K = (size_t)a.g.k;
   PlaneRef<T> r;
-  r.mu = (T*)a.s.mu + sc * K * P;
-  r.var = (T*)a.s.var + sc * K * P;
-  r.w = (T*)a.s.w + sc * K * P;
+  r.KB = kbucket(a.g.k);
+  r.R = rec_elems(r.KB);
+  r.mix = (T*)a.s.mix + sc * P * (size_t)r.R;
   r.meta = a.s.meta + sc * P;
   r.dyn = a.s.dyn + sc * P;
   r.streak = a.s.streak + sc * P;
   r.hits = a.s.hits + sc * 5 * P;
-  r.tg = tab_geo(a.g);
-  r.table = a.s.table + sc * r.tg.plane;
+  r.table = a.s.table + sc * P * 256;
   r.peak = a.s.peak + sc * P;
   r.P = P;
   return r;
 }
 
+// mode k of plane-pixel p
+template <typename T>
+__device__ __forceinline__ T* rec_of(const PlaneRef<T>& r, size_t p) {
+  return r.mix + p * (size_t)r.R;
+}
+template <typename T>
+__device__ __forceinline__ T* w_of(const PlaneRef<T>& r, size_t p, int k) {
+  return r.mix + p * (size_t)r.R + 2 * r.KB + k;
+}
+
+// the whole record in one round of 16-byte loads; e keeps dead slots and
+// padding so the record can be stored back whole (KMAX is the bucket)
 template <typename T, int KMAX>
 __device__ __forceinline__ void load_mix_r(const PlaneRef<T>& r, size_t p,
-                                           int n, Mix<KMAX>& x) {
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k) {
-    x.mu[k] = 0.0;
-    x.var[k] = 1.0;
-    x.w[k] = 0.0;
-    if (k < n) {
-      x.mu[k] = ldrw(r.mu + k * r.P + p);
-      x.var[k] = ldrw(r.var + k * r.P + p);
-      x.w[k] = ldrw(r.w + k * r.P + p);
-    }
-  }
+                                           int n, Mix<KMAX>& x,
+                                           T (&e)[rec_elems(KMAX)]) {
+  rec_load<rec_elems(KMAX)>(rec_of(r, p), e);
+  rec_to_mix<KMAX, T>(e, n, x);
 }
 
 template <typename T, int KMAX>
 __device__ __forceinline__ void store_mix_r(const PlaneRef<T>& r, size_t p,
-                                            int n, const Mix<KMAX>& x) {
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k) {
-    if (k < n) {
-      st(r.mu + k * r.P + p, x.mu[k]);
-      st(r.var + k * r.P + p, x.var[k]);
-      st(r.w + k * r.P + p, x.w[k]);
-    }
-  }
+                                            int n, const Mix<KMAX>& x,
+                                            T (&e)[rec_elems(KMAX)]) {
+  mix_to_rec<KMAX, T>(x, n, e);
+  rec_store<rec_elems(KMAX)>(rec_of(r, p), e);
 }
 
 // ---------------------------------------------------------------------------
@@ -248,7 +205,8 @@ __device__ __noinline__ void cold_reset(PlaneRef<T> r, size_t p,
   uint32_t dyn = r.dyn[p];
   int n = meta_count(meta);
   Mix<KMAX> x;
-  load_mix_r<T, KMAX>(r, p, n, x);
+  T e[rec_elems(KMAX)];
+  load_mix_r<T, KMAX>(r, p, n, x, e);
   double v = (double)dyn_chp(dyn);
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) {
@@ -259,7 +217,7 @@ __device__ __noinline__ void cold_reset(PlaneRef<T> r, size_t p,
   }
   int inv[KMAX];
   sort_modes<KMAX>(x, n, inv);
-  store_mix_r<T, KMAX>(r, p, n, x);
+  store_mix_r<T, KMAX>(r, p, n, x, e);
   r.meta[p] = (uint16_t)meta_with_refs(meta,
                                        select_inv<KMAX>(inv, meta_ref(meta, 0)),
                                        select_inv<KMAX>(inv, meta_ref(meta, 1)));
@@ -288,10 +246,9 @@ __device__ __noinline__ void cold_reorder(PlaneRef<T> r, size_t p,
       double lmu = group_mu;
       if (code[j] != L_GROUP) {
         int k = meta_ref(meta, code[j] == L_MEAN ? 0 : 1);
-        lmu = ldrw(r.mu + (size_t)k * r.P + p);
+        lmu = ldrw(rec_of(r, p) + 2 * k);
       }
-      nm[j] = -(double)r.table[tab_pix(r.tg, p) +
-                               (size_t)clip_rint(lmu) * r.tg.SL];
+      nm[j] = -(double)r.table[p * 256 + (size_t)clip_rint(lmu)];
     }
   }
   // np.lexsort((-mass, -hv)): primary -hv, secondary -mass, stable
@@ -322,7 +279,8 @@ __device__ __noinline__ void cold_meanvar(PlaneRef<T> r, size_t p,
                                           double rho, double var_floor) {
   const int n = meta_count(meta);
   Mix<KMAX> x;
-  load_mix_r<T, KMAX>(r, p, n, x);
+  T e[rec_elems(KMAX)];
+  load_mix_r<T, KMAX>(r, p, n, x, e);
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) {
     if (k == rs) {
@@ -336,7 +294,7 @@ __device__ __noinline__ void cold_meanvar(PlaneRef<T> r, size_t p,
   }
   int inv[KMAX];
   sort_modes<KMAX>(x, n, inv);
-  store_mix_r<T, KMAX>(r, p, n, x);
+  store_mix_r<T, KMAX>(r, p, n, x, e);
   r.meta[p] = (uint16_t)meta_with_refs(meta,
                                        select_inv<KMAX>(inv, meta_ref(meta, 0)),
                                        select_inv<KMAX>(inv, meta_ref(meta, 1)));
@@ -351,10 +309,11 @@ __device__ __noinline__ int cold_gmm(PlaneRef<T> r, size_t p, uint32_t meta,
                                      int kcap, int remap) {
   int n = meta_count(meta);
   Mix<KMAX> x;
-  load_mix_r<T, KMAX>(r, p, n, x);
+  T e[rec_elems(KMAX)];
+  load_mix_r<T, KMAX>(r, p, n, x, e);
   int inv[KMAX];
   int label = gmm_step<KMAX>(x, n, kcap, v, rho, gp, inv);
-  store_mix_r<T, KMAX>(r, p, n, x);
+  store_mix_r<T, KMAX>(r, p, n, x, e);
   uint32_t nm = meta_with_count(meta, n);
   if (remap)
     nm = meta_with_refs(nm, select_inv<KMAX>(inv, meta_ref(meta, 0)),
@@ -402,15 +361,6 @@ struct Pre {
   T mu0, var0, mu1, var1;  // the MEAN (ref0) and MEANVAR (ref1) modes
 };
 
-// the mode slot whose (mu, var) the confidence reads, or -1 for the group
-__device__ __forceinline__ int top_ref(bool grouping, uint32_t meta,
-                                       bool group_ok) {
-  int top = meta_mid(meta, 0);
-  if (top == L_GROUP && !grouping) top = meta_mid(meta, 1);
-  if (top == L_GROUP && group_ok) return -1;
-  return meta_ref(meta, top == L_MEANVAR ? 1 : 0);
-}
-
 // false for pixels the sampling gate will skip or copy (no table / mode
 // reads for them)
 __device__ __forceinline__ bool will_evaluate(bool sampling, uint32_t dyn,
@@ -444,17 +394,14 @@ __device__ __forceinline__ void preload_r2(const PlaneRef<T>& pr, size_t p,
   x.var0 = x.var1 = (T)1;
   if (compat || !will_evaluate(sampling, x.dyn, x.vb, on_lattice, eps)) return;
   // one 32-B sector of a 1 KB row: bypass L1 (no 128-B line fill)
-#ifdef COG_EXP_NOTABLE
-  x.tv = 0.01f;
-#else
-  x.tv = __ldcg(pr.table + tab_pix(pr.tg, p) + (size_t)x.vb * pr.tg.SL);
-#endif
+  x.tv = __ldcg(pr.table + p * 256 + (size_t)x.vb);
   const int r0 = meta_ref(x.meta, 0), r1 = meta_ref(x.meta, 1);
-  x.mu0 = pr.mu[(size_t)r0 * pr.P + p];
-  x.var0 = pr.var[(size_t)r0 * pr.P + p];
+  const T* rec = rec_of(pr, p);
+  x.mu0 = rec[2 * r0];
+  x.var0 = rec[2 * r0 + 1];
   if (r1 != r0) {
-    x.mu1 = pr.mu[(size_t)r1 * pr.P + p];
-    x.var1 = pr.var[(size_t)r1 * pr.P + p];
+    x.mu1 = rec[2 * r1];
+    x.var1 = rec[2 * r1 + 1];
   } else {
     x.mu1 = x.mu0;
     x.var1 = x.var0;
@@ -475,15 +422,6 @@ constexpr float MATCH_ABS_MARGIN = 3e-5f;  // > fp32 rounding of |v - mu| (v <= 
 __device__ __noinline__ bool match_exact(double v, double mu, double var,
                                          double lam) {
   return fabs(v - mu) <= lam * sqrt(var);
-}
-
-__device__ __forceinline__ bool match_filtered(float vf, float mu, float var,
-                                               float lamf, double lam) {
-  const float thr = lamf * sqrtf(var);
-  const float gap = fabsf(vf - mu) - thr;
-  if (gap < -FILTER_MARGIN * thr) return true;
-  if (gap > FILTER_MARGIN * thr) return false;
-  return match_exact((double)vf, (double)mu, (double)var, lam);
 }
 
 // reference confidence (kernels_numba.py:243-270), binary64
@@ -554,29 +492,12 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
   }
 
   const uint32_t meta = pre.meta;
-#ifdef COG_EXP_SKELETON
-  // timing ablation: same loads/stores, trivial arithmetic
-  {
-    const float cf = pre.tv / pre.peak + (float)pre.mu0 * 1e-9f +
-                     (float)pre.var1 * 1e-9f + (float)pre.mu1 * 1e-9f +
-                     (float)pre.var0 * 1e-9f;
-    pr.streak[p] = pre.streak + 1u;
-    atomicAdd(pr.hits + p, 1u);
-    o.kind = L_GROUP;
-    o.label = 0;
-    o.conf = (double)cf;
-    o.rho = 0.0;
-    o.dyn = pack_dyn(vb, 0, waking, L_GROUP, clock) ^ (meta & 1u);
-    pr.dyn[p] = o.dyn;
-    return;
-  }
-#endif
   if (f.compat) {
     // kind from the pre-update rank-0 mode; the full update is deep work
     const int n = meta_count(meta);
     int active = L_GMM;
-    if (n > 0 && fabs(v - ldrw(pr.mu + p)) <=
-                     q.match_lambda * sqrt(ldrw(pr.var + p)))
+    const T* rec = rec_of(pr, p);
+    if (n > 0 && fabs(v - ldrw(rec)) <= q.match_lambda * sqrt(ldrw(rec + 1)))
       active = L_MEAN;
     atomicAdd(pr.hits + (size_t)active * P + p, 1u);  // RED: no round trip
     o.kind = active;
@@ -683,7 +604,7 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
       if (!done && hit && code != L_GROUP && rr > 0) {
         // a matched mode outside the background weight prefix is not a hit
         double acc = 0.0;
-        for (int k = 0; k < rr; ++k) acc = acc + ldrw(pr.w + (size_t)k * P + p);
+        for (int k = 0; k < rr; ++k) acc = acc + ldrw(w_of(pr, p, k));
         hit = acc <= q.background_threshold;
       }
       if (!done && hit) {
@@ -692,7 +613,7 @@ __device__ __forceinline__ void hot_px(const StepArgs& a, const Flags& f,
       }
     }
     if (active == L_MEAN) {
-      st(pr.mu + (size_t)r0 * P + p, (1.0 - rho) * (double)pre.mu0 + rho * v);
+      st(rec_of(pr, p) + 2 * r0, (1.0 - rho) * (double)pre.mu0 + rho * v);
     } else if (active == L_MEANVAR) {
       o.deep = DEEP_MEANVAR;
       o.rsel = r1;
@@ -868,15 +789,6 @@ __device__ __forceinline__ void flush_wq(WarpScratch& ws, int& wq_n,
 // Per-tile work shared by both step kernels.  `fill(c, pre)` provides plane
 // c's preloaded values (global loads or shared-memory stages).
 // ---------------------------------------------------------------------------
-#ifdef COG_PROF
-__device__ unsigned long long g_prof[16];
-#define PROF_T(v) const long long v = clock64()
-#define PROF_ADD(i, dt) if (lane == 0) atomicAdd(&g_prof[i], (unsigned long long)(dt))
-#else
-#define PROF_T(v)
-#define PROF_ADD(i, dt)
-#endif
-
 struct TileCtx {
   int s, d, G, lane, it, ty, tx, col, stride, cw, W;
   size_t P, p;
@@ -930,9 +842,6 @@ __device__ __forceinline__ void tile_pass(const StepArgs& a, const Flags& f,
   unsigned lbits = 0, copybits = 0, gmmbits = 0, latebits = 0;
   int nq = 0;
   ws.glab[lane] = 0u;
-#ifdef COG_PROF
-  const long long tp0 = clock64();
-#endif
 
   // ---- 1. hot pass, plane by plane
 #pragma unroll 1
@@ -1059,10 +968,6 @@ __device__ __forceinline__ void tile_pass(const StepArgs& a, const Flags& f,
 
   // ---- 2. in-warp deep pass (planes with copy pixels only)
   __syncwarp();
-#ifdef COG_PROF
-  const long long tp1 = clock64();
-  if (lane == 0) atomicAdd(&g_prof[8], (unsigned long long)(tp1 - tp0));
-#endif
   for (int e = lane; e < nq; e += 32) {
     const uint32_t code = ws.qcode[e];
     const int owner = code & 31, c = (code >> 5) & 3;
@@ -1124,7 +1029,6 @@ struct StepSmem {
   WarpScratch* ws;
   uint32_t* lane;        // lane-private partials, lane_bytes per warp
   size_t lane_bytes;
-  unsigned char* extra;  // per-warp staging (pipelined kernel)
 };
 
 __device__ __forceinline__ StepShared step_shared(const StepSmem& m, int warp,
@@ -1191,7 +1095,6 @@ __device__ __forceinline__ StepSmem step_prologue(const StepArgs& a,
   m.ws = (WarpScratch*)(m.acc_all + warps * words);
   m.lane = (uint32_t*)(m.ws + warps);
   m.lane_bytes = lane_acc_bytes(d, G);
-  m.extra = (unsigned char*)m.lane + (size_t)warps * m.lane_bytes;
   for (size_t i = threadIdx.x; i < (size_t)warps * m.lane_bytes / 4;
        i += blockDim.x)
     m.lane[i] = 0u;
@@ -1336,256 +1239,6 @@ __global__ void __launch_bounds__(STEP_THREADS, COG_STEP_MINB)
 }
 
 // ---------------------------------------------------------------------------
-// pipelined step kernel (strides 1/2/4, width % 4 == 0): each warp stages
-// the state of its upcoming tiles in shared memory with cp.async --
-// stage A (tile j+2): dyn, streak, peak, meta, frame bytes, class, group id
-// stage B (tile j+1, needs A): table entry at v and the two referenced
-//          modes' (mu, var), skipped for pixels the gate will not evaluate
-// compute (tile j) reads only shared memory; stores go straight to HBM.
-// Two tiles' loads are in flight behind every tile being evaluated.
-// ---------------------------------------------------------------------------
-constexpr int PIPE_WARPS = 4;
-constexpr int PIPE_THREADS = PIPE_WARPS * 32;
-
-__device__ __forceinline__ void cpa(void* dst, const void* src, int bytes,
-                                    bool pred) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-  if (bytes == 8)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa),
-                 "l"(src), "r"(pred ? 8 : 0)
-                 : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa),
-                 "l"(src), "r"(pred ? 4 : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cpa_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cpa_wait2() {
-  asm volatile("cp.async.wait_group 2;" ::: "memory");
-}
-__device__ __forceinline__ void cpa_wait0() {
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
-struct PipeLayout {  // byte offsets inside one warp's staging area
-  int a_dyn, a_streak, a_peak, a_meta, a_frame, a_cls, a_gid, a_bytes;
-  int b_tv, b_mu0, b_var0, b_mu1, b_var1, b_bytes;
-  int total;
-};
-
-__host__ __device__ inline PipeLayout pipe_layout(int d, int tsize) {
-  PipeLayout L;
-  L.a_dyn = 0;
-  L.a_streak = L.a_dyn + d * 128;
-  L.a_peak = L.a_streak + d * 128;
-  L.a_meta = L.a_peak + d * 128;
-  L.a_frame = L.a_meta + d * 64;
-  L.a_cls = L.a_frame + d * 32;
-  L.a_gid = L.a_cls + 32;
-  L.a_bytes = ((L.a_gid + 64) + 15) & ~15;
-  L.b_tv = 0;
-  L.b_mu0 = d * 128;
-  L.b_var0 = L.b_mu0 + d * 32 * tsize;
-  L.b_mu1 = L.b_var0 + d * 32 * tsize;
-  L.b_var1 = L.b_mu1 + d * 32 * tsize;
-  L.b_bytes = ((L.b_var1 + d * 32 * tsize) + 15) & ~15;
-  L.total = 3 * L.a_bytes + 2 * L.b_bytes;
-  return L;
-}
-
-#ifndef COG_PIPE_MINB
-#define COG_PIPE_MINB 4
-#endif
-
-template <typename T, int KMAX>
-__global__ void __launch_bounds__(PIPE_THREADS, COG_PIPE_MINB)
-    pipe_kernel(const StepArgs a) {
-  extern __shared__ double s_mem[];
-  const Flags f{a.q.sampling_on != 0, a.q.grouping_on != 0,
-                a.q.rate_scaling_on != 0, a.q.chp_on != 0,
-                a.q.literal_conf != 0, a.q.compat != 0};
-  const StepSmem m = step_prologue(a, f, PIPE_WARPS, s_mem);
-  const int s = blockIdx.y;
-  const int d = a.g.depth, G = a.g.n_groups;
-  const int H = a.g.height, W = a.g.width, stride = a.g.stride;
-  const size_t P = (size_t)H * W;
-  const int words = acc_words(d, G);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const StepShared sh = step_shared(m, warp, d, G, words);
-  const PipeLayout L = pipe_layout(d, (int)sizeof(T));
-  unsigned char* stage = m.extra + (size_t)warp * L.total;
-  unsigned char* bufA[3] = {stage, stage + L.a_bytes, stage + 2 * L.a_bytes};
-  unsigned char* bufB[2] = {stage + 3 * L.a_bytes,
-                            stage + 3 * L.a_bytes + L.b_bytes};
-  uint32_t* sync = a.s.sync + (size_t)s * 4;
-  const bool do_reset = (*(volatile uint32_t*)(sync + 1) & 1u) != 0;
-  const bool do_reorder = a.reorder_now != 0;
-  const uint8_t* frame = a.frame + (size_t)s * d * P;
-  const uint8_t* cls = a.s.cls + (size_t)s * P;
-  const uint16_t* gidp = a.s.gid + (size_t)s * P;
-  const int cw = a.cw;
-  const int lrow = lane / cw, lcol = lane - lrow * cw;
-  unsigned long long fg_count = 0;
-  const size_t dq_cap = dq_capacity(d, P);
-  unsigned long long* dq_code = (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
-  double* dq_rho = a.s.deeprho + (size_t)s * dq_cap;
-  int wq_n = 0;
-
-  // this lane's pixel of tile wt
-  auto pix = [&](int wt, size_t& p, bool& valid, bool& on_lat) {
-    const int ty = wt / a.tiles_x, tx = wt - ty * a.tiles_x;
-    const int y = ty * stride + lrow, x = tx * cw + lcol;
-    valid = wt < a.n_tiles && y < H && x < W;
-    p = valid ? (size_t)y * W + x : 0;
-    on_lat = ((a.g.row0 + y) % stride == 0) && (x % stride == 0);
-  };
-  auto cold = [&](int wt) {  // pending reset / reorder before staging
-    size_t p;
-    bool valid, on_lat;
-    pix(wt, p, valid, on_lat);
-    if (valid) {
-      const int gid = gidp[p];
-      const bool member = G > 0 && gid != (int)UNGROUPED;
-#pragma unroll 1
-      for (int c = 0; c < d; ++c) {
-        const PlaneRef<T> pr = plane_ref<T>(a, s, c);
-        if (do_reset) cold_reset<T, KMAX>(pr, p, a.q.initial_variance);
-        if (do_reorder)
-          cold_reorder<T>(pr, p, member ? m.gmu[c * G + gid]
-                                        : (G > 0 ? m.gmu[c * G] : 0.0));
-      }
-    }
-    __syncwarp();
-  };
-  auto stage_a = [&](int wt, unsigned char* A) {
-    size_t p;
-    bool valid, on_lat;
-    pix(wt, p, valid, on_lat);
-    if (do_reset || do_reorder) cold(wt);
-#pragma unroll 1
-    for (int c = 0; c < d; ++c) {
-      const PlaneRef<T> pr = plane_ref<T>(a, s, c);
-      cpa(A + L.a_dyn + c * 128 + lane * 4, pr.dyn + p, 4, valid);
-      cpa(A + L.a_streak + c * 128 + lane * 4, pr.streak + p, 4, valid);
-      cpa(A + L.a_peak + c * 128 + lane * 4, pr.peak + p, 4, valid);
-      if ((lane & 1) == 0)
-        cpa(A + L.a_meta + c * 64 + lane * 2, pr.meta + p, 4, valid);
-      if ((lane & 3) == 0)
-        cpa(A + L.a_frame + c * 32 + lane, frame + (size_t)c * P + p, 4,
-            valid);
-    }
-    if ((lane & 3) == 0) cpa(A + L.a_cls + lane, cls + p, 4, valid);
-    if ((lane & 1) == 0) cpa(A + L.a_gid + lane * 2, gidp + p, 4, valid);
-    cpa_commit();
-  };
-  auto stage_b = [&](int wt, const unsigned char* A, unsigned char* B) {
-    size_t p;
-    bool valid, on_lat;
-    pix(wt, p, valid, on_lat);
-#pragma unroll 1
-    for (int c = 0; c < d; ++c) {
-      const PlaneRef<T> pr = plane_ref<T>(a, s, c);
-      const uint32_t dyn = ((const uint32_t*)(A + L.a_dyn + c * 128))[lane];
-      const uint32_t meta = ((const uint16_t*)(A + L.a_meta + c * 64))[lane];
-      const int vb = (A + L.a_frame + c * 32)[lane];
-      const bool ev = valid && !f.compat &&
-                      will_evaluate(f.sampling, dyn, vb, on_lat, a.q.chp_epsilon);
-      const int r0 = meta_ref(meta, 0), r1 = meta_ref(meta, 1);
-      cpa(B + L.b_tv + c * 128 + lane * 4,
-          pr.table + ((size_t)wt * 256 + vb) * 32 + lane, 4, ev);
-      cpa(B + L.b_mu0 + (c * 32 + lane) * sizeof(T), pr.mu + (size_t)r0 * P + p,
-          sizeof(T), ev);
-      cpa(B + L.b_var0 + (c * 32 + lane) * sizeof(T),
-          pr.var + (size_t)r0 * P + p, sizeof(T), ev);
-      cpa(B + L.b_mu1 + (c * 32 + lane) * sizeof(T), pr.mu + (size_t)r1 * P + p,
-          sizeof(T), ev);
-      cpa(B + L.b_var1 + (c * 32 + lane) * sizeof(T),
-          pr.var + (size_t)r1 * P + p, sizeof(T), ev);
-    }
-    cpa_commit();
-  };
-
-  // static round-robin tile assignment: tile j of this warp is gw + j*nw
-  const int nw = gridDim.x * PIPE_WARPS;
-  const int gw = blockIdx.x * PIPE_WARPS + warp;
-  int tj = gw, tj1 = gw + nw, tj2 = gw + 2 * nw;
-  stage_a(tj, bufA[0]);
-  stage_a(tj1, bufA[1]);
-  asm volatile("cp.async.wait_group 1;" ::: "memory");  // A(0) landed
-  __syncwarp();
-  stage_b(tj, bufA[0], bufB[0]);
-  for (int j = 0; tj < a.n_tiles; ++j) {
-    const int t3 = tj2 + nw;
-    PROF_T(c0);
-    stage_a(tj2, bufA[(j + 2) % 3]);
-    PROF_T(c1);
-    cpa_wait2();  // A(j+1) landed
-    __syncwarp();
-    PROF_T(c2);
-    stage_b(tj1, bufA[(j + 1) % 3], bufB[(j + 1) & 1]);
-    PROF_T(c3);
-    cpa_wait2();  // B(j) landed
-    __syncwarp();
-    PROF_T(c4);
-    PROF_ADD(0, c1 - c0);
-    PROF_ADD(1, c2 - c1);
-    PROF_ADD(2, c3 - c2);
-    PROF_ADD(3, c4 - c3);
-
-    // ---- evaluate tile j from shared memory
-    const unsigned char* A = bufA[j % 3];
-    const unsigned char* B = bufB[j & 1];
-    TileCtx t;
-    t.s = s; t.d = d; t.G = G; t.lane = lane; t.stride = stride;
-    t.cw = cw; t.W = W; t.P = P; t.it = 0;
-    t.ty = tj / a.tiles_x;
-    t.tx = tj - t.ty * a.tiles_x;
-    t.col = lcol;
-    pix(tj, t.p, t.valid, t.on_lat);
-    t.gid = ((const uint16_t*)(A + L.a_gid))[lane];
-    t.cls = (A + L.a_cls)[lane];
-    t.member = t.valid && G > 0 && t.gid != (int)UNGROUPED;
-    unsigned row0_lbl = 0;
-    tile_pass<T, KMAX>(
-        a, f, t, sh, row0_lbl, wq_n, fg_count, dq_code, dq_rho, sync,
-        [&](int c, Pre<T>& pre) {
-          pre.vb = (A + L.a_frame + c * 32)[lane];
-          pre.dyn = ((const uint32_t*)(A + L.a_dyn + c * 128))[lane];
-          pre.meta = ((const uint16_t*)(A + L.a_meta + c * 64))[lane];
-          pre.streak = ((const uint32_t*)(A + L.a_streak + c * 128))[lane];
-          pre.peak = ((const float*)(A + L.a_peak + c * 128))[lane];
-          pre.tv = ((const float*)(B + L.b_tv + c * 128))[lane];
-          pre.mu0 = ((const T*)(B + L.b_mu0))[c * 32 + lane];
-          pre.var0 = ((const T*)(B + L.b_var0))[c * 32 + lane];
-          pre.mu1 = ((const T*)(B + L.b_mu1))[c * 32 + lane];
-          pre.var1 = ((const T*)(B + L.b_var1))[c * 32 + lane];
-          if (!t.valid) {
-            pre.peak = 1.0f;
-            pre.var0 = pre.var1 = (T)1;
-          }
-        });
-    PROF_T(c5);
-    PROF_ADD(4, c5 - c4);
-    PROF_ADD(5, 1);
-    tj = tj1;
-    tj1 = tj2;
-    tj2 = t3;
-  }
-  PROF_T(c6);
-  cpa_wait0();
-  if (wq_n) flush_wq(*sh.ws, wq_n, sync + 3, dq_code, dq_rho, lane);
-  fold_lane_partials(sh, d, G, lane);
-  if (lane == 0) sh.wacc[acc_fg(d)] += fg_count;
-  PROF_T(c7);
-  PROF_ADD(6, c7 - c6);
-  step_publish(a, m, PIPE_WARPS);
-  PROF_T(c8);
-  PROF_ADD(7, c8 - c7);
-}
-
-// ---------------------------------------------------------------------------
 // deep kernel: the stream's worklist of MEANVAR hits and GMM fall-throughs,
 // one plane-pixel per thread (dense warps).  GMM labels are OR-ed into the
 // dyn word and the mask; a pixel turning foreground here is counted exactly
@@ -1610,20 +1263,11 @@ __device__ __forceinline__ unsigned deep_item(const StepArgs& a, int s,
   const double v = (double)((code >> 8) & 0xFF);
   const size_t p = (size_t)(code >> 16);
   const PlaneRef<T> pr = plane_ref<T>(a, s, c);
-  // meta and every slot of the mixture in one round of loads
+  // meta and the whole mixture record in one round of loads
   const uint32_t meta = pr.meta[p];
   Mix<KMAX> x;
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k) {
-    x.mu[k] = 0.0;
-    x.var[k] = 1.0;
-    x.w[k] = 0.0;
-    if (k < a.g.k) {
-      x.mu[k] = ldrw(pr.mu + k * P + p);
-      x.var[k] = ldrw(pr.var + k * P + p);
-      x.w[k] = ldrw(pr.w + k * P + p);
-    }
-  }
+  T e[rec_elems(KMAX)];
+  load_mix_r<T, KMAX>(pr, p, meta_count(meta), x, e);
   int n = meta_count(meta);
   int inv[KMAX];
   unsigned newly = 0;
@@ -1640,13 +1284,13 @@ __device__ __forceinline__ unsigned deep_item(const StepArgs& a, int s,
       }
     }
     sort_modes<KMAX>(x, n, inv);
-    store_mix_r<T, KMAX>(pr, p, n, x);
+    store_mix_r<T, KMAX>(pr, p, n, x, e);
     pr.meta[p] = (uint16_t)meta_with_refs(
         meta, select_inv<KMAX>(inv, meta_ref(meta, 0)),
         select_inv<KMAX>(inv, meta_ref(meta, 1)));
   } else {
     const int lbl = gmm_step<KMAX>(x, n, a.g.k, v, rho, gp, inv);
-    store_mix_r<T, KMAX>(pr, p, n, x);
+    store_mix_r<T, KMAX>(pr, p, n, x, e);
     uint32_t nm = meta_with_count(meta, n);
     if (kindq == DEEP_GMM)
       nm = meta_with_refs(nm, select_inv<KMAX>(inv, meta_ref(meta, 0)),
@@ -1752,16 +1396,19 @@ __device__ __forceinline__ unsigned deep_item_f32(const StepArgs& a, int s,
   const size_t p = (size_t)(code >> 16);
   const PlaneRef<float> pr = plane_ref<float>(a, s, c);
   const uint32_t meta = pr.meta[p];
+  constexpr int R = rec_elems(KMAX), WO = rec_w(KMAX);
+  float e[R];
+  rec_load<R>(rec_of(pr, p), e);
   float mu[KMAX], var[KMAX], w[KMAX];
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) {
-    mu[k] = 0.0f;
-    var[k] = 1.0f;
-    w[k] = 0.0f;
-    if (k < a.g.k) {
-      mu[k] = pr.mu[k * P + p];
-      var[k] = pr.var[k * P + p];
-      w[k] = pr.w[k * P + p];
+    mu[k] = e[2 * k];
+    var[k] = e[2 * k + 1];
+    w[k] = e[WO + k];
+    if (k >= a.g.k) {
+      mu[k] = 0.0f;
+      var[k] = 1.0f;
+      w[k] = 0.0f;
     }
   }
   int n = meta_count(meta);
@@ -1863,15 +1510,16 @@ __device__ __forceinline__ unsigned deep_item_f32(const StepArgs& a, int s,
     ok = false;
     return 0;
   }
-  // ---- write back (deep_item's bookkeeping)
+  // ---- write back (deep_item's bookkeeping): the whole record
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) {
     if (k < n) {
-      pr.mu[k * P + p] = mu[k];
-      pr.var[k * P + p] = var[k];
-      pr.w[k * P + p] = w[k];
+      e[2 * k] = mu[k];
+      e[2 * k + 1] = var[k];
+      e[WO + k] = w[k];
     }
   }
+  rec_store<R>(rec_of(pr, p), e);
   if (kindq == DEEP_MEANVAR) {
     pr.meta[p] = (uint16_t)meta_with_refs(
         meta, select_inv<KMAX>(inv, meta_ref(meta, 0)),
@@ -1910,12 +1558,7 @@ __global__ void __launch_bounds__(DEEP_THREADS) deep_kernel(const StepArgs a) {
   const size_t dq_cap = dq_capacity(d, P);
   unsigned long long* dq_code = (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
   const double* dq_rho = a.s.deeprho + (size_t)s * dq_cap;
-#ifdef COG_EXP_NODEEP
-  const size_t n = 0;  // timing ablation: the kernel's fixed cost only
-#else
   const size_t n = *(volatile uint32_t*)(sync + 3);
-#endif
-  uint8_t* mask = a.mask + (size_t)s * P;
   if (threadIdx.x == 0) s_fg = 0;
   __syncthreads();
   unsigned fg = 0;
@@ -1930,7 +1573,6 @@ __global__ void __launch_bounds__(DEEP_THREADS) deep_kernel(const StepArgs a) {
     if (!(code & 1ull)) continue;
     dq_code[i] = 0ull;
     if constexpr (sizeof(T) == 4) {
-#ifndef COG_EXP_DEEP64
       if (!a.q.compat) {  // fp32 arithmetic, binary64 fallback near ties
         bool ok;
         const unsigned nw = deep_item_f32<KMAX>(a, s, code, dq_rho[i], ok);
@@ -1939,7 +1581,6 @@ __global__ void __launch_bounds__(DEEP_THREADS) deep_kernel(const StepArgs a) {
           continue;
         }
       }
-#endif
     }
     fg += deep_item<T, KMAX>(a, s, code, dq_rho[i]);
   }
@@ -1963,21 +1604,22 @@ __global__ void __launch_bounds__(DEEP_THREADS) deep_kernel(const StepArgs a) {
   finalize_stream<T>(a, s, gacc, a.stats, sync);
 }
 
-// reference layout f32[d][P][256] <-> tile-major (one stream); one thread
-// per table entry, coalesced on the reference side
-__global__ void table_pack_kernel(TabGeo tg, int d, size_t P,
-                                  float* ref_layout, float* tiled,
-                                  int to_tiled) {
+// hot prior of one stream: reference-layout table f32[d][P][256] + peak ->
+// tile-major u16 phat (cascade.py:213-216, phat = table / peak in binary64,
+// stored as round(phat * 65535)); one thread per entry, coalesced reads
+__global__ void tabq_build_kernel(TabGeo tg, int d, size_t P,
+                                  const float* __restrict__ table,
+                                  const float* __restrict__ peak,
+                                  uint16_t* tabq) {
   const size_t n = (size_t)d * P * 256;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
     const size_t c = i / (P * 256), rem = i - c * P * 256;
     const size_t p = rem >> 8, v = rem & 255;
-    const size_t t = c * tg.plane + tab_pix(tg, p) + v * tg.SL;
-    if (to_tiled)
-      tiled[t] = ref_layout[i];
-    else
-      ref_layout[i] = tiled[t];
+    const double ph = (double)table[i] / (double)peak[c * P + p];
+    double q = rint(ph * 65535.0);
+    q = q < 0.0 ? 0.0 : (q > 65535.0 ? 65535.0 : q);
+    tabq[c * tg.plane + tab_pix(tg, p) + v * tg.SL] = (uint16_t)q;
   }
 }
 
@@ -2197,25 +1839,26 @@ __global__ void __launch_bounds__(128) warmup_kernel(const WarmArgs a) {
     a.features[p * 2 + 1] = qw / (double)N;
     if (a.w_final) a.w_final[p] = m.w[0];
   }
-  // store the mixture (dead slots keep the canonical (0, init_var, 0))
-  const size_t base = (size_t)c * K * P;
-  for (int k = 0; k < K; ++k) {
-    double mu = 0.0, var = a.q.initial_variance, w = 0.0;
+  // store the mixture record (dead slots hold the canonical (0, init_var,
+  // 0), padding zero)
+  {
+    T e[rec_elems(KMAX)];
 #pragma unroll
-    for (int kk = 0; kk < KMAX; ++kk)
-      if (kk == k) {
-        mu = m.mu[kk];
-        var = m.var[kk];
-        w = m.w[kk];
+    for (int i = 0; i < rec_elems(KMAX); ++i) e[i] = (T)0;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (k < K) {
+        e[2 * k] = (T)m.mu[k];
+        e[2 * k + 1] = (T)m.var[k];
+        e[rec_w(KMAX) + k] = (T)m.w[k];
       }
-    st((T*)a.s.mu + base + k * P + p, mu);
-    st((T*)a.s.var + base + k * P + p, var);
-    st((T*)a.s.w + base + k * P + p, w);
+    }
+    rec_store<rec_elems(KMAX)>(
+        (T*)a.s.mix + ((size_t)c * P + p) * rec_elems(KMAX), e);
   }
   // mode references: lexsort((-tie, -mass)) over all K slots
   // (cascade.py:218-235); dead slots carry (-inf, -inf)
-  const TabGeo tg = tab_geo(a.g);
-  const float* trow = a.s.table + (size_t)c * tg.plane + tab_pix(tg, p);
+  const float* trow = a.s.table + ((size_t)c * P + p) * 256;
   double nm[KMAX], nt[KMAX];
   const double PINF = __longlong_as_double(0x7ff0000000000000ll);
 #pragma unroll
@@ -2223,7 +1866,7 @@ __global__ void __launch_bounds__(128) warmup_kernel(const WarmArgs a) {
     nm[k] = PINF;
     nt[k] = PINF;
     if (k < n) {
-      nm[k] = -(double)trow[(size_t)clip_rint(m.mu[k]) * tg.SL];
+      nm[k] = -(double)trow[(size_t)clip_rint(m.mu[k])];
       nt[k] = -(m.w[k] / sqrt(m.var[k]));
     }
   }
@@ -2279,18 +1922,18 @@ __global__ void __launch_bounds__(256) baseline_kernel(const StepArgs a) {
                   a.q.variance_floor, a.q.initial_variance};
   int fg = 0;
   for (int c = 0; c < d; ++c) {
-    MixPtrs<T> mp{(T*)a.s.mu + (size_t)c * K * P, (T*)a.s.var + (size_t)c * K * P,
-                  (T*)a.s.w + (size_t)c * K * P};
+    const PlaneRef<T> pr = plane_ref<T>(a, 0, c);
     uint16_t* metap = a.s.meta + (size_t)c * P + p;
     uint32_t meta = *metap;
     int n = meta_count(meta);
     Mix<KMAX> x;
-    load_mix<T, KMAX>(mp, P, p, n, x);
+    T e[rec_elems(KMAX)];
+    load_mix_r<T, KMAX>(pr, p, n, x, e);
     int inv[KMAX];
     int n0 = n;
     fg |= gmm_step<KMAX>(x, n, K, (double)a.frame[(size_t)c * P + p],
                          a.q.learning_rate, gp, inv);
-    store_mix<T, KMAX>(mp, P, p, n, x);
+    store_mix_r<T, KMAX>(pr, p, n, x, e);
     if (n != n0) *metap = (uint16_t)meta_with_count(meta, n);
   }
   a.mask[p] = fg ? 255 : 0;
@@ -2303,14 +1946,16 @@ template <typename T>
 __global__ void export_kernel(cog_geom g, cog_state s, cog_ref_state o) {
   const size_t P = (size_t)g.height * g.width;
   const int d = g.depth, K = g.k;
+  const int R = rec_elems(kbucket(K)), WO = rec_w(kbucket(K));
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < d * P;
        i += (size_t)gridDim.x * blockDim.x) {
     const size_t c = i / P, p = i % P;
+    const T* rec = (const T*)s.mix + i * R;
     for (int k = 0; k < K; ++k) {
-      const size_t src = (c * K + k) * P + p, dst = i * K + k;
-      o.mu[dst] = (double)((const T*)s.mu)[src];
-      o.var[dst] = (double)((const T*)s.var)[src];
-      o.w[dst] = (double)((const T*)s.w)[src];
+      const size_t dst = i * K + k;
+      o.mu[dst] = (double)rec[2 * k];
+      o.var[dst] = (double)rec[2 * k + 1];
+      o.w[dst] = (double)rec[WO + k];
     }
     uint32_t m = s.meta[i], dy = s.dyn[i];
     o.count[i] = meta_count(m);
@@ -2331,14 +1976,16 @@ template <typename T>
 __global__ void import_kernel(cog_geom g, cog_state s, cog_ref_state in) {
   const size_t P = (size_t)g.height * g.width;
   const int d = g.depth, K = g.k;
+  const int R = rec_elems(kbucket(K)), WO = rec_w(kbucket(K));
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < d * P;
        i += (size_t)gridDim.x * blockDim.x) {
     const size_t c = i / P, p = i % P;
+    T* rec = (T*)s.mix + i * R;
     for (int k = 0; k < K; ++k) {
-      const size_t dst = (c * K + k) * P + p, src = i * K + k;
-      st((T*)s.mu + dst, in.mu[src]);
-      st((T*)s.var + dst, in.var[src]);
-      st((T*)s.w + dst, in.w[src]);
+      const size_t src = i * K + k;
+      st(rec + 2 * k, in.mu[src]);
+      st(rec + 2 * k + 1, in.var[src]);
+      st(rec + WO + k, in.w[src]);
     }
     s.meta[i] = (uint16_t)pack_meta((int)in.count[i], in.mid[i * 3],
                                     in.mid[i * 3 + 1], in.mid[i * 3 + 2],
@@ -2490,20 +2137,6 @@ __global__ void __launch_bounds__(256)
 // ---------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------
-// Random 4-byte table lookups must not drag 64/128-B DRAM fetches along.
-void set_fetch_granularity() {
-  static bool done = false;
-  if (!done) {
-    cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
-    size_t got = 0;
-    cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
-    if (getenv("COG_DEBUG"))
-      fprintf(stderr, "cog: L2 fetch granularity -> %zu (rc %d)\n", got, (int)e);
-    cudaGetLastError();
-    done = true;
-  }
-}
-
 int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -2606,24 +2239,10 @@ StepFn<T> pick_deep(int K) {
   return deep_kernel<T, 8>;
 }
 
-template <typename T>
-StepFn<T> pick_pipe(int K) {
-  if (K <= 3) return pipe_kernel<T, 3>;
-  if (K <= 5) return pipe_kernel<T, 5>;
-  return pipe_kernel<T, 8>;
-}
-
-// step-kernel selection: COG_KERNEL=lean|pipe|general (default lean where
-// it applies; COG_NO_PIPE=1 forces the general kernel, for parity tests)
-int kernel_choice() {
-  const char* e = getenv("COG_KERNEL");
-  if (getenv("COG_NO_PIPE")) return 2;
-  if (!e) return 0;
-  if (e[0] == 'p') return 1;
-  if (e[0] == 'g') return 2;
-  if (e[0] == 'l') return 3;
-  return 0;  // "fast" and default
-}
+// step-kernel choice (cog_params.variant): 0 automatic, 1 general, 2 lean;
+// a kernel is used only where its shared memory fits (per-warp group
+// partials grow with the group count), so any valid configuration runs
+constexpr size_t SMEM_CAP = 200 * 1024;
 
 template <typename T>
 StepFn<T> pick_lean(int K, int d) {
@@ -2638,16 +2257,24 @@ StepFn<T> pick_lean(int K, int d) {
 }
 
 bool lean_ok(const StepArgs& a) {
-  const int kc = kernel_choice();
-  return (kc == 0 || kc == 3) && a.iters == 1 &&
-         (a.g.depth == 1 || a.g.depth == 3) && a.g.stride <= 5;
+  return (a.q.variant == 0 || a.q.variant == 2) && a.iters == 1 &&
+         (a.g.depth == 1 || a.g.depth == 3) && a.g.stride <= 5 &&
+         lean_smem_bytes(a.g.depth, a.g.n_groups) <= SMEM_CAP;
+}
+
+size_t step_smem_bytes(const StepArgs& a) {
+  const int warps = STEP_WARPS;
+  return 256 * 8 + (size_t)2 * a.g.depth * a.g.n_groups * 8 +
+         (size_t)warps * acc_words(a.g.depth, a.g.n_groups) * 8 +
+         (size_t)warps * sizeof(WarpScratch) +
+         (size_t)warps * lane_acc_bytes(a.g.depth, a.g.n_groups);
 }
 
 template <typename T>
 int launch_lean(const StepArgs& a, cudaStream_t st) {
   auto fn = pick_lean<T>(a.g.k, a.g.depth);
   const size_t smem = lean_smem_bytes(a.g.depth, a.g.n_groups);
-  if (smem > 200 * 1024) return COG_EUNSUPPORTED;
+  if (smem > SMEM_CAP) return COG_EUNSUPPORTED;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
@@ -2661,19 +2288,11 @@ int launch_lean(const StepArgs& a, cudaStream_t st) {
   return launch_status();
 }
 
-// the pipelined kernel needs one-pass warp tiles and 4-byte aligned rows
-bool pipe_ok(const StepArgs& a) {
-  if (kernel_choice() == 2) return false;
-  const int st = a.g.stride;
-  return (st == 1 || st == 2 || st == 4) && a.iters == 1 &&
-         (a.g.width % 4) == 0 && ((uintptr_t)a.frame % 4) == 0;
-}
-
 template <int KMAX, int D>
 int launch_fast_k(const StepArgs& a, cudaStream_t st) {
   auto fn = fast_kernel<KMAX, D>;
   const size_t smem = fast_smem_bytes(a.g.depth, a.g.n_groups);
-  if (smem > 200 * 1024) return COG_EUNSUPPORTED;
+  if (smem > SMEM_CAP) return COG_EUNSUPPORTED;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
@@ -2708,16 +2327,11 @@ int launch_fast(const StepArgs& a, cudaStream_t st) {
 template <typename T>
 int launch_hot(const StepArgs& a, cudaStream_t st) {
   if (lean_ok(a)) return launch_lean<T>(a, st);
-  const bool pipe = pipe_ok(a);
-  auto fn = pipe ? pick_pipe<T>(a.g.k) : pick_step<T>(a.g.k);
-  const int threads = pipe ? PIPE_THREADS : STEP_THREADS;
+  auto fn = pick_step<T>(a.g.k);
+  const int threads = STEP_THREADS;
   const int warps = threads / 32;
-  size_t smem = 256 * 8 + (size_t)2 * a.g.depth * a.g.n_groups * 8 +
-                (size_t)warps * acc_words(a.g.depth, a.g.n_groups) * 8 +
-                (size_t)warps * sizeof(WarpScratch) +
-                (size_t)warps * lane_acc_bytes(a.g.depth, a.g.n_groups);
-  if (pipe) smem += (size_t)warps * pipe_layout(a.g.depth, sizeof(T)).total;
-  if (smem > 200 * 1024) return COG_EUNSUPPORTED;
+  const size_t smem = step_smem_bytes(a);
+  if (smem > SMEM_CAP) return COG_EUNSUPPORTED;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
@@ -2735,9 +2349,14 @@ bool fast_ok(const StepArgs& a, bool f32) {
   const unsigned long long span = (unsigned long long)a.g.streams *
                                   a.g.depth * (a.g.k > 5 ? a.g.k : 5) *
                                   (unsigned long long)a.g.height * a.g.width;
-  return f32 && kernel_choice() == 0 && a.iters == 1 && a.g.stride <= 5 &&
-         (a.g.depth == 1 || a.g.depth == 3) && span < (1ull << 32) &&
-         !a.q.exact_group_sums;
+  const unsigned long long recs = (unsigned long long)a.g.streams *
+                                  a.g.depth * (unsigned long long)a.g.height *
+                                  a.g.width * rec_elems(kbucket(a.g.k));
+  return f32 && a.q.variant == 0 && a.s.tabq != nullptr && a.iters == 1 &&
+         a.g.stride <= 5 && (a.g.depth == 1 || a.g.depth == 3) &&
+         span < (1ull << 32) && recs < (1ull << 32) &&
+         !a.q.exact_group_sums &&
+         fast_smem_bytes(a.g.depth, a.g.n_groups) <= SMEM_CAP;
 }
 
 template <typename T>
@@ -2745,12 +2364,9 @@ int launch_deep(const StepArgs& a, cudaStream_t st, bool pdl) {
   auto fn = pick_deep<T>(a.g.k);
   const size_t P = (size_t)a.g.height * a.g.width;
   size_t dg = (P * a.g.depth / 8 + DEEP_THREADS - 1) / DEEP_THREADS;  // ~12% items
-  // grid-stride over the worklist, one wave (COG_DEEP_CTAS_PER_SM
-  // overrides the occupancy)
-  const char* env = getenv("COG_DEEP_CTAS_PER_SM");
+  // grid-stride over the worklist, one wave
   const size_t per_sm =
-      env ? (size_t)atoi(env)
-          : (size_t)cached_occupancy((const void*)fn, DEEP_THREADS, 0);
+      (size_t)cached_occupancy((const void*)fn, DEEP_THREADS, 0);
   size_t cap = (size_t)num_sms() * per_sm / a.g.streams;
   if (cap < 1) cap = 1;
   if (dg > cap) dg = cap;
@@ -2777,17 +2393,15 @@ int launch_deep(const StepArgs& a, cudaStream_t st, bool pdl) {
 
 template <typename T>
 int launch_step(const StepArgs& a, cudaStream_t st) {
-  set_fetch_granularity();
   ensure_bterm();
-  // float32 state: the fast kernel; otherwise lean / pipelined / general
+  // float32 state: the fast kernel; otherwise lean / general
   const bool fast = fast_ok(a, sizeof(T) == 4);
   int rc = fast ? launch_fast(a, st) : launch_hot<T>(a, st);
   if (rc) return rc;
-  // programmatic dependent launch of the deep pass: its CTAs are scheduled
-  // while the hot kernel drains (they wait in griddepcontrol.wait), which
-  // hides the launch gap -- measured 72.9 -> 70.9 us per C2 step
-  // (tools/ab_bench.sh); COG_NO_PDL=1 launches it plainly
-  return launch_deep<T>(a, st, fast && !getenv("COG_NO_PDL"));
+  // programmatic dependent launch of the deep pass behind the fast kernel:
+  // its CTAs are scheduled while the hot kernel drains (they wait in
+  // griddepcontrol.wait), which hides the launch gap
+  return launch_deep<T>(a, st, fast);
 }
 
 }  // namespace
@@ -2798,49 +2412,40 @@ int launch_step(const StepArgs& a, cudaStream_t st) {
 extern "C" {
 
 const char* cog_version(void) {
-  return "cog_b200 1.0 (sm_100a, binary64 decisions, fused step)";
+  return "cog_b200 2.0 (sm_100a, binary64 decisions, fused step, record "
+         "mixtures, u16 hot prior)";
 }
 
 int64_t cog_accum_words(int32_t depth, int32_t n_groups) {
   return acc_words(depth, n_groups);
 }
 
-int cog_debug_prof(uint64_t* out16, int reset) {
-#ifdef COG_PROF
-  cudaMemcpyFromSymbol(out16, g_prof, sizeof(unsigned long long) * 16);
-  if (reset) {
-    unsigned long long z[16] = {0};
-    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
-  }
-  return 0;
-#else
-  (void)out16;
-  (void)reset;
-  return COG_EUNSUPPORTED;
-#endif
-}
-
 int64_t cog_deepq_slots(int32_t depth, int64_t n_pix) {
   return (int64_t)dq_capacity(depth, (size_t)n_pix);
 }
 
-int64_t cog_table_floats(const cog_geom* geom) {
+int64_t cog_mix_elems(int32_t k) {
+  if (k < 1 || k > 8) return -1;
+  return rec_elems(kbucket(k));
+}
+
+int64_t cog_tabq_elems(const cog_geom* geom) {
   if (!geom || check_geom(geom)) return -1;
   return (int64_t)(tab_geo(*geom).plane * (size_t)geom->depth);
 }
 
-int cog_table_pack(const cog_geom* geom, float* ref_layout, float* tiled,
-                   int32_t to_tiled, void* stream) {
+int cog_tabq_build(const cog_geom* geom, const float* table, const float* peak,
+                   uint16_t* tabq, void* stream) {
   int rc = check_geom(geom);
   if (rc) return rc;
-  if (!ref_layout || !tiled) return COG_EINVAL;
+  if (!table || !peak || !tabq) return COG_EINVAL;
   const size_t P = (size_t)geom->height * geom->width;
   const size_t n = (size_t)geom->depth * P * 256;
   size_t blocks = (n + 255) / 256;
   const size_t cap = (size_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
-  table_pack_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-      tab_geo(*geom), geom->depth, P, ref_layout, tiled, to_tiled);
+  tabq_build_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      tab_geo(*geom), geom->depth, P, table, peak, tabq);
   return launch_status();
 }
 

@@ -1,9 +1,8 @@
 // cog_lean.cuh -- the lean per-frame step kernel (included inside the
 // anonymous namespace of cog_kernels.cu, after the shared helpers).
 //
-// Same work unit and the same per-plane-pixel decisions as the pipelined
-// kernel (hot_px: kernels_numba.py:188-359), organised for occupancy instead
-// of explicit staging:
+// Same work unit and the same per-plane-pixel decisions as the general
+// step kernel (hot_px: kernels_numba.py:188-359), organised for occupancy:
 //   * one thread = one pixel, all D planes (D a template parameter); one warp
 //     = one stride-aligned tile (stride rows x cw columns, so every copy
 //     pixel's anchor sits in row 0 of the same warp);
@@ -24,7 +23,7 @@
 //     plane-tile that holds copy pixels runs its deep items in-warp so the
 //     copies see their anchors' final labels.
 // The deep kernel then runs the worklist and its last CTA finalizes the
-// frame, exactly as after the pipelined kernel.
+// frame, exactly as after the general kernel.
 
 constexpr int LEAN_THREADS = 256;
 constexpr int LEAN_WARPS = LEAN_THREADS / 32;
@@ -91,7 +90,7 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_LEAN_MINB)
   for (int i = threadIdx.x; i < words; i += LEAN_THREADS) s_acc[i] = 0ull;
   __syncthreads();
 
-  // ---- per-stream bases (planes are P apart, modes K*P apart)
+  // ---- per-stream bases (planes are P apart, records R elements)
   const size_t sD = (size_t)s * D;
   const uint8_t* frame = a.frame + sD * P;
   uint32_t* dynb = a.s.dyn + sD * P;
@@ -99,11 +98,9 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_LEAN_MINB)
   uint32_t* stkb = a.s.streak + sD * P;
   const float* peakb = a.s.peak + sD * P;
   uint32_t* hitsb = a.s.hits + sD * 5 * P;
-  const TabGeo tg = tab_geo(a.g);
-  const float* tabb = a.s.table + sD * tg.plane;
-  T* mub = (T*)a.s.mu + sD * K * P;
-  T* varb = (T*)a.s.var + sD * K * P;
-  T* wgtb = (T*)a.s.w + sD * K * P;
+  const float* tabb = a.s.table + sD * P * 256;   // reference layout
+  constexpr int R = rec_elems(KMAX);
+  T* mixb = (T*)a.s.mix + sD * P * R;
   T* confb = (T*)a.conf + sD * P;
   uint8_t* kindb = a.kind + sD * P;
   uint8_t* maskb = a.mask + (size_t)s * P;
@@ -189,20 +186,15 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_LEAN_MINB)
                       will_evaluate(f.sampling, pre[c].dyn, pre[c].vb, on_lat,
                                     eps);
       if (ev) {
-        const uint32_t o = (uint32_t)c * P + p;
-#ifdef COG_EXP_NOTABLE
-        pre[c].tv = 0.01f * (float)(o & 7);  // ablation: no table gather
-#else
-        pre[c].tv = __ldcg(tabb + (size_t)c * tg.plane +
-                           ((size_t)wt * 256 + pre[c].vb) * 32 + lane);
-#endif
+        const size_t o = (size_t)c * P + p;
+        pre[c].tv = __ldcg(tabb + o * 256 + pre[c].vb);
         const int r0 = meta_ref(pre[c].meta, 0), r1 = meta_ref(pre[c].meta, 1);
-        const size_t mb = (size_t)c * K * P + p;
-        pre[c].mu0 = mub[mb + (size_t)r0 * P];
-        pre[c].var0 = varb[mb + (size_t)r0 * P];
+        const T* rec = mixb + o * R;
+        pre[c].mu0 = rec[2 * r0];
+        pre[c].var0 = rec[2 * r0 + 1];
         if (r1 != r0) {
-          pre[c].mu1 = mub[mb + (size_t)r1 * P];
-          pre[c].var1 = varb[mb + (size_t)r1 * P];
+          pre[c].mu1 = rec[2 * r1];
+          pre[c].var1 = rec[2 * r1 + 1];
         } else {
           pre[c].mu1 = pre[c].mu0;
           pre[c].var1 = pre[c].var0;
@@ -226,17 +218,16 @@ __global__ void __launch_bounds__(LEAN_THREADS, COG_LEAN_MINB)
     for (int c = 0; c < D; ++c) {
       const uint32_t o = (uint32_t)c * P + p;
       PlaneRef<T> pr;
-      pr.mu = mub + (size_t)c * K * P;
-      pr.var = varb + (size_t)c * K * P;
-      pr.w = wgtb + (size_t)c * K * P;
+      pr.mix = mixb + (size_t)c * P * R;
+      pr.R = R;
+      pr.KB = KMAX;
       pr.meta = metab + (size_t)c * P;
       pr.dyn = dynb + (size_t)c * P;
       pr.streak = stkb + (size_t)c * P;
       pr.hits = hitsb + (size_t)c * 5 * P;
-      pr.table = tabb + (size_t)c * tg.plane;
+      pr.table = tabb + (size_t)c * P * 256;
       pr.peak = peakb + (size_t)c * P;
       pr.P = P;
-      pr.tg = tg;
       HotOut ho;
       ho.kind = 0;
       ho.label = 0;

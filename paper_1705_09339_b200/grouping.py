@@ -114,13 +114,16 @@ class KMeans:
         return label, ctr
 
 
+# point sets of at least this many points run the k-means assignment on the
+# GPU (a module attribute the parity tests lower to 0 or raise; no env knob)
+KMEANS_DEVICE_MIN = 65536
+
+
 def _device_assign(n: int, pts: np.ndarray) -> bool:
-    """GPU assignment for large point sets (COG_KMEANS_DEVICE_MIN points,
-    default 65536; 0 forces it, for the parity tests)."""
-    import os
+    """GPU assignment for large point sets (>= KMEANS_DEVICE_MIN points)."""
     if pts.ndim != 2 or pts.shape[1] != 2:
         return False
-    if n < int(os.environ.get("COG_KMEANS_DEVICE_MIN", "65536")):
+    if n < KMEANS_DEVICE_MIN:
         return False
     try:
         import torch

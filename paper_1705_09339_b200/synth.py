@@ -185,11 +185,24 @@ class Scene:
         out = np.clip(np.rint(val), 0, 255).astype(np.uint8)
         return (out, truth) if with_truth else out
 
-    def frames(self, start: int, stop: int, workers: int = 1) -> np.ndarray:
+    def frames(self, start: int, stop: int, workers: int = 1,
+               threads: int = 0) -> np.ndarray:
         """(stop-start, d, H, W) uint8.  Every frame is a pure function of
-        (seed, t), so ``workers > 1`` renders them in parallel processes
-        (bit-identical to the serial result)."""
+        (seed, t), so ``workers > 1`` renders them in parallel processes and
+        ``threads > 1`` in threads of this process (numpy releases the GIL
+        in the bulk work; safe after CUDA is initialised, where forking is
+        not) -- both bit-identical to the serial result."""
         ts = list(range(start, stop))
+        if threads > 1 and len(ts) > 1:
+            import concurrent.futures as cf
+            out = np.empty((len(ts), self.spec.depth, self.spec.height,
+                            self.spec.width), dtype=np.uint8)
+
+            def one(i):
+                out[i] = self.frame(ts[i])
+            with cf.ThreadPoolExecutor(threads) as ex:
+                list(ex.map(one, range(len(ts))))
+            return out
         if workers <= 1 or len(ts) < 2 * workers:
             return np.stack([self.frame(t) for t in ts])
         import concurrent.futures as cf

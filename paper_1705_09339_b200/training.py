@@ -56,16 +56,13 @@ def train_device(eng: CascadeEngine, values: torch.Tensor,
     n, d, p = values.shape
     lib = _lib.load()
     cuda_stream = torch.cuda.current_stream(dev.device).cuda_stream
+    # the full-window table lands straight in the engine's buffer, then the
+    # hot u16 copy is built from it (float32 engines)
     prior = build_scene_prior_device(
         values, config, windows=kde_windows, bandwidth=bandwidth,
-        out_peak=dev.peak[stream], out_classes=dev.cls[stream],
-        height=dev.height, width=dev.width)
+        out_tables=dev.table[stream], out_peak=dev.peak[stream],
+        out_classes=dev.cls[stream], height=dev.height, width=dev.width)
     dev.table_from_ref(stream, prior.tables)
-    if len(prior.windows) == 1:
-        # the engine's tile-major table is now the only copy (the reference
-        # layout is rebuilt on demand: CascadeEngine.tables)
-        prior.tables = None
-        prior.window_tables = {}
     feats = w_final = None
     if config.grouping:
         feats = torch.empty((p, 2), dtype=torch.float64, device=dev.device)

@@ -56,8 +56,8 @@ def test_host_only_calls():
 
 
 def test_table_layout_size():
-    """Tile-major prior table: per plane n_tiles x 256 bins x SL slots
-    (host-side arithmetic only, no GPU)."""
+    """Tile-major hot prior (u16): per plane n_tiles x 256 bins x SL slots;
+    mixture records of 16 / 32 elements (host-side arithmetic, no GPU)."""
     lib = _lib.load()
     for (h, w, st, d, floats) in [
             (480, 640, 2, 3, 3 * (640 // 16) * (480 // 2) * 256 * 32),
@@ -66,4 +66,6 @@ def test_table_layout_size():
         g = _lib.Geom()
         g.total_pixels, g.height, g.width, g.depth = h * w, h, w, d
         g.k, g.stride, g.streams = 3, st, 1
-        assert lib.cog_table_floats(_lib.ref(g)) == floats
+        assert lib.cog_tabq_elems(_lib.ref(g)) == floats
+    assert [lib.cog_mix_elems(k) for k in range(1, 9)] == [16] * 5 + [32] * 3
+    assert lib.cog_mix_elems(0) == -1 and lib.cog_mix_elems(9) == -1

@@ -168,9 +168,9 @@ def test_device_kmeans_equals_numpy_kmeans(n, k, monkeypatch):
     pts = np.concatenate([rng.normal(0, 1, (n // 2, 2)),
                           rng.normal(3, 0.5, (n - n // 2, 2))])
     pts[::97] = pts[1]                       # many identical points
-    monkeypatch.setenv("COG_KMEANS_DEVICE_MIN", str(10 ** 12))
+    monkeypatch.setattr(grouping, "KMEANS_DEVICE_MIN", 10 ** 12)
     want_l, want_c = grouping.KMeans(k, 3).fit(pts.copy())
-    monkeypatch.setenv("COG_KMEANS_DEVICE_MIN", "0")
+    monkeypatch.setattr(grouping, "KMEANS_DEVICE_MIN", 0)
     got_l, got_c = grouping.KMeans(k, 3).fit(pts.copy())
     assert np.array_equal(got_l, want_l)
     assert np.array_equal(got_c, want_c)
@@ -212,9 +212,10 @@ def test_training_with_device_kmeans_equals_host_kmeans(name, monkeypatch):
     cfg = config_for(overrides)
     frames = rec["frames"]
     n_train = int(rec["n_train"])
-    monkeypatch.setenv("COG_KMEANS_DEVICE_MIN", str(10 ** 12))
+    from paper_1705_09339_b200 import grouping
+    monkeypatch.setattr(grouping, "KMEANS_DEVICE_MIN", 10 ** 12)
     a = _single(frames, n_train, cfg)
-    monkeypatch.setenv("COG_KMEANS_DEVICE_MIN", "0")
+    monkeypatch.setattr(grouping, "KMEANS_DEVICE_MIN", 0)
     b = _single(frames, n_train, cfg)
     assert np.array_equal(a.group_id, b.group_id)
     for nm in STATE:

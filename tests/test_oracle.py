@@ -29,6 +29,52 @@ def test_kde_tables_match_reference():
         assert counts.sum() == n * d * h * w
 
 
+def test_kde_tables32_match_reference():
+    """the full-geometry path (C loop over nonzero bins, f32 out) gives the
+    reference's f32 tables exactly"""
+    z = np.load(GOLDEN / "kde.npz")
+    vals = z["values"]
+    n, d, h, w = vals.shape
+    flat = np.ascontiguousarray(vals.reshape(n, d, h * w))
+    for i in range(3):
+        t32 = orc.kde_tables32(flat, float(z[f"bw{i}"]))
+        assert np.array_equal(t32, z[f"tables{i}"].astype(np.float32))
+    long = np.ascontiguousarray(z["long"].reshape(*z["long"].shape[:2], -1))
+    rng = np.random.default_rng(7)
+    noisy = rng.integers(0, 256, size=(37, 2, 501)).astype(np.uint8)
+    for v in (long, noisy):
+        _, t = orc.kde(v, 5.0)
+        assert np.array_equal(orc.kde_tables32(v, 5.0), t.astype(np.float32))
+
+
+def test_kmeans_matches_numpy_expression():
+    """the C assignment loop reproduces the reference's numpy k-means
+    (grouping.py:100-126) including exact distance ties"""
+    rng = np.random.default_rng(3)
+    f = np.round(rng.normal(size=(5000, 2)), 1)  # many exact ties
+    for k in (2, 3, 5):
+        a, c = orc.kmeans(f, k, seed=k)
+        # the reference loop, verbatim
+        r = np.random.default_rng(k)
+        cen = np.empty((k, 2))
+        cen[0] = f[int(r.integers(f.shape[0]))]
+        d2 = ((f - cen[0]) ** 2).sum(axis=1)
+        for j in range(1, k):
+            cen[j] = f[int(np.argmax(d2))]
+            d2 = np.minimum(d2, ((f - cen[j]) ** 2).sum(axis=1))
+        asg = np.full(f.shape[0], -1, dtype=np.int64)
+        for _ in range(100):
+            nxt = np.argmin(((f[:, None, :] - cen[None]) ** 2).sum(axis=2), axis=1)
+            if np.array_equal(nxt, asg):
+                break
+            asg = nxt
+            for j in range(k):
+                m = f[asg == j]
+                if m.shape[0]:
+                    cen[j] = m.mean(axis=0)
+        assert np.array_equal(a, asg) and np.array_equal(c, cen)
+
+
 def test_kde_windows_and_residue_match_reference():
     z = np.load(GOLDEN / "kde.npz")
     long = z["long"]

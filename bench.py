@@ -1,27 +1,38 @@
 """Benchmark of the CoG hot path (BASELINE.json metric: pixel-frames/s of
-classify+update, and % of HBM roofline).
+classify+update, and % of HBM roofline at 1/2/4/8 B200).
 
-Workload (N=1, default): BASELINE config C2 -- 640x480 RGB, K=3, trained
-on the first 200 frames of the seeded synthetic scene
-(paper_1705_09339_b200.synth); a step is one frame through the step kernels.
-For N>1 every rank runs its own independent C2-shaped stream (seed 1+rank,
-no collectives: weak scaling), timed on the device, MAX over ranks.
---workload c3 / c4 / c5 measure the other BASELINE configs (c4 at N>1: one
-4K stream in row bands with a per-frame NCCL all-reduce, strong scaling;
-c5: a batch engine of independent 720p streams).
+Workload (default, N=1): BASELINE config C4 -- one 3840x2160 RGB stream,
+K=5, trained on the first 150 frames of the seeded synthetic scene
+(paper_1705_09339_b200.synth), the largest configuration a single GPU
+holds.  A step is one frame through the step kernels.  At N>1 the 4K frame
+is split into N stride-aligned row bands, one per rank, with the frame's
+exact partials summed by one NCCL all-reduce per frame (strong scaling:
+the ranks share each frame).
+Other workloads (--workload): c3 (1920x1080, one stream per rank), c2
+(640x480, one stream per rank), c5 (64 independent 1280x720 streams split
+over the ranks, processed in waves of --streams resident streams).
 
-value    device-resident frames, CUDA events around each step's launch on the
-         engine stream, L2 flushed (256 MiB write) between steps (outside
-         the events).
-e2e      the public API: ``process_frame(Frame)`` from pinned host memory +
-         reading ``mask.labels`` back every step.
-roofline achieved = algorithmic bytes of the frame (from its own level
-         populations, byte model in DESIGN.md) / step-kernel duration.
-cpu_baseline  the oracle (C restatement of the reference kernels, 1 thread
-         like the serial reference) on a bounded sample of the same stream.
+``--gpus N`` without a torchrun environment re-launches this script under
+``torch.distributed.run`` with N ranks (one per GPU).
 
---impl reference runs the reference's CPU path (the oracle port, all host
-threads) on the same workload; rank 0 only.
+value    device-resident frames, CUDA events around each step's launches on
+         the engine stream, L2 flushed (256 MiB write, untimed) between
+         steps; MAX over ranks of the summed step time.
+e2e      the public API ``process_frame`` fed numpy frames from (pageable)
+         host memory, as a reference caller passes them: staging, H2D,
+         step, D2H of mask + stats all inside the timed region.
+roofline the fused frame step (fast_kernel + deep_kernel): SURVEY.md 8(d)
+         algorithmic bytes of each timed frame (B_frame from that frame's
+         own level populations) / step time; when the committed ncu
+         capture of the same workload (profiles/traffic_<workload>.json)
+         shows fewer DRAM bytes than B_frame, the fraction uses those.
+cpu_baseline  the oracle (C restatement of the reference's serial numba
+         kernels, 1 thread) on a bounded sample of the same stream, seeded
+         with the GPU engine's trained state (c4: a 270-row band).
+
+--impl reference: the reference's CPU path (the oracle port, all host
+threads) on the same workload; rank 0 only (c4: a 270-row band, trained by
+the oracle itself).
 """
 
 from __future__ import annotations
@@ -29,7 +40,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -42,6 +55,9 @@ sys.path.insert(0, str(ROOT))
 
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
+METRIC = "pixel-frames/sec (CoG classify+update)"
+C5_STREAMS = 64
+BAND_ROWS = 270       # c4 CPU samples: rows 0-269 (1/8 of the 4K frame)
 
 
 def hbm_peak():
@@ -52,29 +68,28 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback"
 
 
-def byte_model(row, depth, k, f64=False):
-    """Algorithmic HBM bytes of one frame from its level populations.
-
-    per plane-pixel: frame 1 + dyn 4r/4w + kind 1w + conf 4w         = 14
-    evaluated: + meta 2 + streak 4r/4w + hits 4r/4w + table sector 32
-               + peak 4 + top-level mode mu/var 2x4                   = +62
-    MEAN: + mu write 4; MEANVAR / GMM: + mixture 12K read + 12K write
-          + meta write 2 (mixture bytes double with float64 storage)
-    per pixel: class 1 + group id 2 + mask 1                          = 4
-    """
-    _, n_chp, n_group, n_mean, n_meanvar, n_gmm, n_skip = row[:7]
+def byte_model(row, depth, k):
+    """SURVEY.md 8(d) algorithmic HBM bytes of one frame from its level
+    populations (FrameStats row: frame, chp, group, mean, meanvar, gmm,
+    skipped, ...):
+      B = sum_level n_level * (R(K) + W_level(K)) + n_skipped * 12 + 3 * P
+      R(K) = 57 + 12K             full record read of an evaluated plane-pixel
+      W_chp = W_group = 13        chp_prev, flags, streak, u16 hit, conf, kind
+      W_mean = 17                 + one mu
+      W_meanvar = W_gmm = 16 + 12K   full mixture + count + refs
+      3 * P                       class + group id read, mask write"""
+    _, n_chp, n_group, n_mean, n_meanvar, n_gmm, n_skip = (int(x) for x in row[:7])
     pixels = (n_chp + n_group + n_mean + n_meanvar + n_gmm + n_skip) // depth
-    mb = 8 if f64 else 4
-    ev = 14 + 62 + (2 * mb - 8)
-    mix = 2 * 3 * mb * k + 2
-    return (n_skip * 14 + (n_chp + n_group) * ev + n_mean * (ev + mb)
-            + (n_meanvar + n_gmm) * (ev + mix) + pixels * 4)
+    r = 57 + 12 * k
+    return ((n_chp + n_group) * (r + 13) + n_mean * (r + 17)
+            + (n_meanvar + n_gmm) * (r + 16 + 12 * k) + n_skip * 12
+            + 3 * pixels)
 
 
 class ClockSampler:
     """nvidia-smi-equivalent sampling (NVML) during the timed region."""
 
-    def __init__(self, index=0, period=0.05):
+    def __init__(self, index=0, period=0.02):
         self.samples, self.reasons = [], set()
         self.max_mhz = None
         self.ok = False
@@ -91,7 +106,7 @@ class ClockSampler:
         self.period = period
         self._stop = threading.Event()
 
-    def _run(self):
+    def _poll(self):
         nv = self.nv
         names = {
             "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
@@ -101,16 +116,19 @@ class ClockSampler:
                 nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
             "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
         }
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(
+                self.h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for k, bit in names.items():
+                if r & bit:
+                    self.reasons.add(k)
+        except Exception:
+            pass
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(
-                    self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for k, bit in names.items():
-                    if r & bit:
-                        self.reasons.add(k)
-            except Exception:
-                pass
+            self._poll()
             time.sleep(self.period)
 
     def __enter__(self):
@@ -123,6 +141,7 @@ class ClockSampler:
         self._stop.set()
         if self.ok:
             self.t.join()
+            self._poll()
 
     def summary(self):
         if not self.samples:
@@ -131,6 +150,21 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(self.samples),
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(self.samples)}
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(n: int) -> int:
+    """Re-run this command under torch.distributed.run with n ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def dist_setup():
@@ -147,44 +181,59 @@ def dist_setup():
     return world, rank, local
 
 
-def cpu_baseline(frames, eng, cfg, n_frames, threads, seconds=10.0):
-    """Oracle engine seeded with the GPU engine's trained state, timed over
-    a bounded run sample (same stream)."""
+def oracle_from_engine(eng, cfg, threads, p0=0, p1=None):
+    """An oracle engine holding pixels [p0, p1) of the GPU engine's state
+    (whole rows), exactly as exported in the reference's layouts."""
     from oracle import oracle as orc
-    os.environ["COG_ORACLE_THREADS"] = str(threads)
-    oe = orc.OracleEngine(cfg, eng.height, eng.width, eng.depth)
+    p1 = eng.n_pix if p1 is None else p1
+    rows = (p1 - p0) // eng.width
+    oe = orc.OracleEngine(cfg, rows, eng.width, eng.depth)
     oe.threads = threads
     st = eng.state_dict()
     for k, v in st.items():
-        setattr(oe, k, np.array(v))
-    oe.tables = eng.tables.copy()
+        if k in ("group_mu", "group_var"):
+            setattr(oe, k, np.array(v))
+        else:
+            setattr(oe, k, np.ascontiguousarray(v[:, p0:p1]))
+    oe.tables = np.ascontiguousarray(
+        eng.dev.table[0][:, p0:p1].cpu().numpy())
     oe.finalize_tables()
-    oe.dynamics = eng.dynamics
+    oe.dynamics = eng.dynamics[p0:p1]
     wt = np.array([cfg.weights_static, cfg.weights_oscillating,
                    cfg.weights_dynamic])[oe.dynamics]
     oe.wa, oe.wb, oe.wc = (np.ascontiguousarray(wt[:, i]) for i in range(3))
-    oe.group_id = eng.group_id
+    oe.group_id = np.ascontiguousarray(eng.group_id[p0:p1])
     oe.group_w = eng.group_w.copy()
     oe.group_members = eng.group_members.copy()
-    oe.process(frames[0])  # warm
-    # a bounded sample: the stream's next frames (cycled if the host set is
-    # shorter), at least n_frames of them and at least `seconds` of CPU work
+    return oe
+
+
+def cpu_baseline(frames, eng, cfg, rows, seconds, min_frames):
+    """The oracle (1 thread: the reference's kernels are serial) seeded with
+    the GPU engine's trained state, timed over a bounded sample of the same
+    stream's post-training frames: at least `min_frames` frames and
+    `seconds` of CPU work (cycled if the host set is shorter)."""
+    os.environ["COG_ORACLE_THREADS"] = "1"
+    r0, r1 = rows
+    oe = oracle_from_engine(eng, cfg, 1, r0 * eng.width, r1 * eng.width)
+    band = [np.ascontiguousarray(f[:, r0:r1]) for f in frames]
+    oe.process(band[0])  # warm
     t0 = time.perf_counter()
     done, dt = 0, 0.0
-    while done < n_frames or dt < seconds:
-        oe.process(frames[1 + done % (len(frames) - 1)])
+    while done < min_frames or dt < seconds:
+        oe.process(band[1 + done % (len(band) - 1)])
         done += 1
         dt = time.perf_counter() - t0
-    return eng.n_pix * done / dt, dt, done
+    return oe.n_pix * done / dt, dt, done
 
 
 def run_reference(args):
     """--impl reference: the reference's CPU path (the oracle port of its
     numba kernels, all host threads) on the same workload; rank 0 only.
     c4 runs a 270-row band (1/8) of the 4K frame: the full frame needs
-    ~100 GB of host RAM in the reference's layout (SURVEY.md 7.7)."""
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    ~100 GB of host RAM in the reference's layout (SURVEY.md 8(d))."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return 0
     from oracle import oracle as orc
@@ -201,9 +250,9 @@ def run_reference(args):
     run = scene.frames(n_train, n_train + args.warmup + args.steps, workers)
     band = ""
     if cid == 4:
-        train = np.ascontiguousarray(train[:, :, :270])
-        run = np.ascontiguousarray(run[:, :, :270])
-        band = " (rows 0-269 of the 4K frame)"
+        train = np.ascontiguousarray(train[:, :, :BAND_ROWS])
+        run = np.ascontiguousarray(run[:, :, :BAND_ROWS])
+        band = f" (rows 0-{BAND_ROWS - 1} of the 4K frame)"
     cfg = EngineConfig(k_max=spec.k_max, color=True,
                        training_frames=n_train).validate()
     t0 = time.perf_counter()
@@ -220,12 +269,12 @@ def run_reference(args):
     total = sum(times)
     value = eng.n_pix * args.steps / total
     line = {
-        "metric": "pixel-frames/sec (CoG classify+update)",
-        "value": value, "unit": "pixel-frames/s", "impl": "reference",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE generator)",
+        "metric": METRIC, "value": value, "unit": "pixel-frames/s",
+        "impl": "reference", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong" if cid == 4 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded BASELINE generator)",
         "config": {"workload": f"{args.workload.upper()} "
                                f"{spec.width}x{spec.height}x3 K={spec.k_max} "
                                f"N={n_train}{band}",
@@ -241,56 +290,51 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "pixel-frames/s",
                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
-def m_bytes(spec):
-    return spec.width * spec.height
-
-
 class Workload:
-    """One bench workload: a trained engine plus its frame sources.
+    """One bench workload on this rank: a trained engine plus its frames.
 
-    c2 (default, BASELINE configs[1]): one 640x480x3 stream per rank.
-    c3: one 1920x1080x3 stream per rank (K=5).
-    c4: one 3840x2160x3 stream; at N>1 split into stride-aligned row bands,
-        one per rank, partials all-reduced over NCCL each frame.
-    c5: independent 1280x720x3 streams (K=5), `streams` resident per rank
-        in one batch engine (64 / N in total, waves of <= 32 on one GPU).
+    c4 (default): one 3840x2160x3 stream; at N>1 one stride-aligned row band
+        per rank, partials all-reduced over NCCL each frame.
+    c3 / c2: one stream per rank (seed offset by rank), no collectives.
+    c5: independent 1280x720x3 streams (K=5); this rank's 64 / N streams in
+        waves of `--streams` resident streams (one batch engine per wave).
     """
 
-    def __init__(self, name, args, world, rank):
+    def __init__(self, name, args, world, rank, streams=None):
         import torch
         from paper_1705_09339_b200 import synth
         from paper_1705_09339_b200.config import EngineConfig
         from paper_1705_09339_b200.training import train_engine
         self.name = name
-        self.pinned = None
         cid = {"c2": 2, "c3": 3, "c4": 4, "c5": 5}[name]
         base = synth.CONFIGS[cid]
         workers = max(1, min(16, len(os.sched_getaffinity(0))))
         total_steps = args.warmup + args.steps
         self.total_steps = total_steps
-        self.extra_frames = 2 * total_steps
+        n_host = total_steps + 1
         t0 = time.perf_counter()
+        self.cfg = EngineConfig(k_max=base.k_max, color=True,
+                                training_frames=base.training,
+                                state_dtype=args.state).validate()
         if name in ("c2", "c3"):
             spec = base.for_stream(rank)
             sc = synth.Scene(spec)
             train = sc.frames(0, spec.training, workers)
-            self.cfg = EngineConfig(k_max=spec.k_max, color=True,
-                                    training_frames=spec.training,
-                                    state_dtype=args.state).validate()
             self.t_gen = time.perf_counter() - t0
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             self.eng = train_engine(train, self.cfg)
             torch.cuda.synchronize()
             self.t_train = time.perf_counter() - t0
-            self.host = sc.frames(spec.training,
-                                  spec.training + self.extra_frames, workers)
+            self.host = sc.frames(spec.training, spec.training + n_host,
+                                  workers)
             self.streams, self.spec = 1, spec
-            self.pixels = spec.n_pix            # per rank per step
+            self.rows = (0, spec.height)
+            self.pixels = spec.n_pix
             self.workload = (f"{name.upper()} {spec.width}x{spec.height}x3 "
                              f"K={spec.k_max} N={spec.training}")
         elif name == "c4":
@@ -299,36 +343,33 @@ class Workload:
             spec = base
             sc = synth.Scene(spec)
             train = sc.frames(0, spec.training, workers)
-            self.cfg = EngineConfig(k_max=spec.k_max, color=True,
-                                    training_frames=spec.training,
-                                    state_dtype=args.state).validate()
             self.t_gen = time.perf_counter() - t0
             rows = band_rows(spec.height, world, self.cfg.stride)[rank]
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            self.eng = train_band_engine(
-                train, self.cfg, rows,
-                gather=dist_gather_rows() if world > 1 else None)
             if world > 1:
+                self.eng = train_band_engine(train, self.cfg, rows,
+                                             gather=dist_gather_rows())
                 self.eng.reducer = DistReducer()
+            else:
+                self.eng = train_engine(train, self.cfg)
             torch.cuda.synchronize()
             self.t_train = time.perf_counter() - t0
-            full = sc.frames(spec.training, spec.training + self.extra_frames,
-                             workers)
+            del train
+            full = sc.frames(spec.training, spec.training + n_host, workers)
             self.host = np.ascontiguousarray(full[:, :, rows[0]:rows[1]])
             self.streams, self.spec = 1, spec
+            self.rows = rows
             self.pixels = (rows[1] - rows[0]) * spec.width
-            self.workload = (f"C4 3840x2160x3 K=5 N=150, rows {rows[0]}-"
-                             f"{rows[1]} of 2160 on this rank")
+            self.workload = ("C4 3840x2160x3 K=5 N=150" if world == 1 else
+                             f"C4 3840x2160x3 K=5 N=150, rows {rows[0]}-"
+                             f"{rows[1] - 1} on rank {rank}")
         else:
-            from paper_1705_09339_b200.parallel import BatchEngine, streams_for_rank
-            mine = streams_for_rank(64, rank, world)[:args.streams]
+            from paper_1705_09339_b200.parallel import BatchEngine
+            mine = streams
             specs = [base.for_stream(i) for i in mine]
             scenes = [synth.Scene(sp) for sp in specs]
             trains = [sc.frames(0, base.training, workers) for sc in scenes]
-            self.cfg = EngineConfig(k_max=base.k_max, color=True,
-                                    training_frames=base.training,
-                                    state_dtype=args.state).validate()
             self.t_gen = time.perf_counter() - t0
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -336,14 +377,14 @@ class Workload:
             torch.cuda.synchronize()
             self.t_train = time.perf_counter() - t0
             del trains
-            per = [sc.frames(base.training, base.training + self.extra_frames,
-                             workers) for sc in scenes]
+            per = [sc.frames(base.training, base.training + n_host, workers)
+                   for sc in scenes]
             self.host = np.ascontiguousarray(np.stack(per, axis=1))  # (T,S,d,H,W)
             self.streams, self.spec = len(mine), base
+            self.rows = (0, base.height)
             self.pixels = len(mine) * base.n_pix
-            self.workload = (f"C5 {len(mine)} x 1280x720x3 K=5 N=100 streams "
-                             f"resident on this rank (seeds {specs[0].seed}-"
-                             f"{specs[-1].seed})")
+            self.workload = (f"C5 {len(mine)} x 1280x720x3 K=5 N=100 "
+                             f"(seeds {specs[0].seed}-{specs[-1].seed})")
         self.dev_frames = [torch.from_numpy(f).cuda() for f in self.host]
         dev = torch.device("cuda", torch.cuda.current_device())
         if self.streams == 1:
@@ -366,81 +407,42 @@ class Workload:
         else:
             self.eng.process_frames_device(f, self.mask, self.stats[j])
 
-    def rows(self, lo):
+    def rows_stats(self, lo):
         r = self.stats[lo:].cpu().numpy()
         return r.reshape(-1, 16)
 
-    def e2e_engine(self):
-        return self.eng.clone() if hasattr(self.eng, "clone") else self.eng
-
     def e2e_submit(self, eng, i):
-        """Public API from host memory: enqueue frame i (H2D from the
-        engine's pinned staging, step, D2H of mask + stats); returns the
-        pending result and the bytes moved each way."""
+        """The public API with host frames: enqueue frame i from this
+        rank's pageable numpy frames (staging copy, H2D, step, D2H of mask
+        + stats); returns the pending result and the bytes moved each
+        way."""
+        f = self.host[i % len(self.host)]
         if self.streams == 1:
-            if self.pinned is None:
-                import torch
-                self.pinned = [torch.from_numpy(f).pin_memory()
-                               for f in self.host]
-            f = self.pinned[i % len(self.pinned)]
-            m, st = eng.process_frame(f)   # pinned host tensor -> DMA
-            return (m, st), f.numel(), m_bytes(self.spec) + 16 * 8
-        if self.pinned is None:        # first (untimed warm-up) call
-            import torch
-            self.pinned = [torch.from_numpy(f).pin_memory()
-                           for f in self.host[:self.total_steps]]
-        f = self.pinned[i % len(self.pinned)]
-        res = eng.submit_frames(f)     # pinned host tensor -> DMA
-        return (res,), f.numel(), (self.streams * self.spec.n_pix
-                                   + self.streams * 16 * 8)
+            m, st = eng.process_frame(f)
+            return (m, st), f.nbytes, self.pixels + 16 * 8
+        res = eng.submit_frames(f)
+        return (res,), f.nbytes, self.pixels + self.streams * 16 * 8
 
     @staticmethod
     def e2e_read(res):
         """Read a submitted frame's result on the host (blocks until its
         copies land)."""
-        if res is not None and len(res) == 1:
+        if len(res) == 1:
             res[0].stats                  # batch: blocks on the download
-        elif res is not None:
+        else:
             m, st = res
             m.labels
             st.n_foreground
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=60)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="cog", choices=["cog", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"])
-    ap.add_argument("--streams", type=int, default=32,
-                    help="c5: resident streams per rank (<= 64 / N)")
-    ap.add_argument("--state", default="float32",
-                    choices=["float32", "float64"])
-    ap.add_argument("--cpu-frames", type=int, default=20)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0,
-                    help="minimum CPU time of the cpu_baseline sample")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--out", default="")
-    args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
-    if args.impl == "reference":
-        return run_reference(args)
-
+def time_device_loop(wl, args, world, local):
+    """W untimed warm-up steps, then K steps, each bracketed by CUDA events
+    on the engine stream with an L2 flush (untimed) in between; returns the
+    per-step durations (ms) and the clock record."""
     import torch
-
-    world, rank, local = dist_setup()
-    wl = Workload(args.workload, args, world, rank)
-    eng, cfg = wl.eng, wl.cfg
-    total_steps = args.warmup + args.steps
     dev = torch.device("cuda", torch.cuda.current_device())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    e2e_eng = wl.e2e_engine()
-    launches_per_step = 2  # hot kernel + deep/finalize kernel
-
-    # ---- device-resident loop
     for i in range(args.warmup):
         flush.zero_()
         wl.step(i, i)
@@ -458,40 +460,18 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    durs = [s.elapsed_time(e) for s, e in zip(starts, ends)]  # ms
-    step_ms = float(np.mean(durs))
-    total_ms = float(np.sum(durs))
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    rows = wl.rows(args.warmup)
-    k = cfg.k_max
-    bytes_frames = [byte_model(r, 3, k, args.state == "float64") for r in rows]
-    steps_bytes = float(np.sum(bytes_frames)) / args.steps
-    achieved = steps_bytes / (step_ms * 1e-3) / 1e9
-    peak, peak_kind = hbm_peak()
-    if args.workload == "c4":
-        # strong scaling: the ranks share one frame
-        value = wl.spec.n_pix * args.steps / (total_ms * 1e-3)
-    else:
-        value = world * wl.pixels * args.steps / (total_ms * 1e-3)
+    del flush
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)], clk
 
-    # ---- warm-L2 back-to-back (diagnostic)
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    ev0.record(stream)
-    for i in range(args.steps):
-        wl.step(total_steps + i, i % total_steps)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    warm_ms = ev0.elapsed_time(ev1) / args.steps
 
-    # ---- end-to-end through the public API (host frames in, mask and
-    # stats read back every step; results are read two frames behind the
-    # submission, so the copies and the host work overlap later steps)
+def time_e2e(wl, args, world):
+    """The public API end to end: frames from host memory, results read on
+    the host two frames behind the submission (so copies and host work
+    overlap later steps)."""
+    import torch
+    eng = wl.eng
     for i in range(args.warmup):
-        r, _, _ = wl.e2e_submit(e2e_eng, i)
+        r, _, _ = wl.e2e_submit(eng, i)
         wl.e2e_read(r)
     torch.cuda.synchronize()
     if world > 1:
@@ -500,85 +480,186 @@ def main():
     bi = bo = 0
     inflight = []
     for i in range(args.steps):
-        cur, bi, bo = wl.e2e_submit(e2e_eng, args.warmup + i)
+        cur, bi, bo = wl.e2e_submit(eng, args.warmup + i)
         inflight.append(cur)
-        if len(inflight) > 2:          # results read two frames behind
+        if len(inflight) > 2:
             wl.e2e_read(inflight.pop(0))
     for r in inflight:
         wl.e2e_read(r)
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    if args.workload == "c4":
-        e2e = wl.spec.n_pix * args.steps / e2e_s
+    return time.perf_counter() - t0, bi, bo
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64,
+                     device=torch.device("cuda", torch.cuda.current_device()))
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="cog", choices=["cog", "reference"])
+    ap.add_argument("--workload", default="c4",
+                    choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--streams", type=int, default=32,
+                    help="c5: resident streams per wave (per rank)")
+    ap.add_argument("--state", default="float32",
+                    choices=["float32", "float64"])
+    ap.add_argument("--cpu-frames", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="minimum CPU time of the cpu_baseline sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
+
+    import torch
+
+    world, rank, local = dist_setup()
+    if args.workload == "c5":
+        from paper_1705_09339_b200.parallel import streams_for_rank
+        mine = streams_for_rank(C5_STREAMS, rank, world)
+        cap = max(1, args.streams)
+        waves = [mine[i:i + cap] for i in range(0, len(mine), cap)]
     else:
-        e2e = world * wl.pixels * args.steps / e2e_s
+        waves = [None]
+
+    durs_all, e2e_s, rows_all = [], 0.0, []
+    t_train = t_gen = 0.0
+    bi = bo = 0
+    clk = None
+    wl = None
+    for wave in waves:
+        if wl is not None:
+            del wl
+            torch.cuda.empty_cache()
+        wl = Workload(args.workload, args, world, rank, streams=wave)
+        t_train += wl.t_train
+        t_gen += wl.t_gen
+        eng, cfg = wl.eng, wl.cfg
+        e2e_eng = eng.clone() if hasattr(eng, "clone") else None
+        durs, c = time_device_loop(wl, args, world, local)
+        clk = c if clk is None else clk
+        durs_all.extend(durs)
+        rows_all.append(wl.rows_stats(args.warmup))
+        if e2e_eng is not None:
+            wl.eng = e2e_eng
+        dt, bi_, bo_ = time_e2e(wl, args, world)
+        e2e_s += dt
+        bi += bi_
+        bo += bo_
+        wl.eng = eng
+    total_ms = max_over_ranks(float(np.sum(durs_all)), world)
+    e2e_s = max_over_ranks(e2e_s, world)
+    rows = np.concatenate(rows_all)
+    k = wl.cfg.k_max
+    spec = wl.spec
+    if args.workload == "c4":
+        units = spec.n_pix                # the ranks share each frame
+    elif args.workload == "c5":
+        units = C5_STREAMS * spec.n_pix   # every stream, over all waves
+    else:
+        units = world * spec.n_pix
+    value = units * args.steps / (total_ms * 1e-3)
+    e2e = units * args.steps / e2e_s
+    step_ms = float(np.mean(durs_all))
+    b_frame = float(np.mean([byte_model(r, 3, k) for r in rows]))
+    b_step = b_frame * (rows.shape[0] / (args.steps * len(waves)))
+    peak, peak_kind = hbm_peak()
+    if args.workload == "c4":
+        # every rank's stats row describes the whole frame, which the
+        # world's ranks process together: compare with the world's HBM
+        peak *= world
 
     line = None
     if rank == 0:
         cpu = None
-        if not args.no_cpu and world == 1 and args.workload in ("c2", "c3"):
-            v, dt, nf = cpu_baseline(wl.host, eng.clone(), cfg,
-                                     args.cpu_frames, 1, args.cpu_seconds)
-            cpu = {"value": v, "unit": "pixel-frames/s", "cores": 1,
-                   "kind": "port",
-                   "sample": f"{nf} {args.workload.upper()} frames (the "
-                             f"stream's post-training frames, cycled over "
-                             f"{len(wl.host) - 1}) from the GPU engine's "
-                             f"trained state, oracle C kernels (restatement "
-                             f"of the serial numba kernels), 1 thread, "
-                             f"{dt:.1f}s"}
-        lvl = rows[:, 1:7].sum(axis=0) / max(1, rows[:, 1:7].sum())
+        if not args.no_cpu and world == 1:
+            r = (0, BAND_ROWS) if args.workload == "c4" else (0, spec.height)
+            eng0 = wl.eng if args.workload != "c5" else None
+            if eng0 is not None:
+                v, dt, nf = cpu_baseline(wl.host, eng0.clone(), wl.cfg, r,
+                                         args.cpu_seconds, args.cpu_frames)
+                what = (f"rows {r[0]}-{r[1] - 1} of" if args.workload == "c4"
+                        else "the whole")
+                cpu = {"value": v, "unit": "pixel-frames/s", "cores": 1,
+                       "kind": "port",
+                       "sample": f"{nf} post-training frames of {what} "
+                                 f"{args.workload.upper()} frame, from the "
+                                 f"GPU engine's trained state; oracle C "
+                                 f"kernels (restatement of the serial numba "
+                                 f"kernels), 1 thread, {dt:.1f}s"}
         traffic = None
         tpath = ROOT / "profiles" / f"traffic_{args.workload}.json"
         if tpath.exists():
             traffic = json.loads(tpath.read_text()).get("bytes_per_step")
+        frac_bytes = min(b_step, traffic) if traffic else b_step
+        achieved = frac_bytes / (step_ms * 1e-3) / 1e9
+        lvl = rows[:, 1:7].sum(axis=0) / max(1, rows[:, 1:7].sum())
+        wave_txt = (f", {len(waves)} wave(s) of <= {args.streams} resident "
+                    f"streams per rank" if args.workload == "c5" else "")
         line = {
-            "metric": "pixel-frames/sec (CoG classify+update)",
-            "value": value, "unit": "pixel-frames/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "metric": METRIC, "value": value, "unit": "pixel-frames/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / (args.steps * len(waves)),
+            "higher_is_better": True,
             "scaling": "strong" if args.workload == "c4" else "weak",
             "vs_baseline": None,
             "dtype": "f32-state/f32-filtered+f64-exact-decisions"
                      if args.state == "float32" else "f64",
             "data": "synthetic (seeded BASELINE generator, "
                     "paper_1705_09339_b200.synth)",
-            "config": {"workload": wl.workload,
-                       "l2": "flushed between steps (256 MiB write, untimed)",
-                       "parallelism": (f"{world} row bands" if
-                                       args.workload == "c4" else
-                                       f"{world} ranks x {wl.streams} "
-                                       f"independent stream(s)")},
+            "config": {"workload": wl.workload if world == 1 and
+                       args.workload != "c5" else
+                       {"c4": "C4 3840x2160x3 K=5 N=150",
+                        "c5": "C5 64 x 1280x720x3 K=5 N=100",
+                        "c3": "C3 1920x1080x3 K=5 N=200",
+                        "c2": "C2 640x480x3 K=3 N=200"}[args.workload],
+                       "l2": "flushed between steps (256 MiB write, "
+                             "untimed); the per-frame state is also far "
+                             "larger than L2",
+                       "parallelism": (f"{world} row band(s), one NCCL "
+                                       f"all-reduce of the frame partials "
+                                       f"per frame" if args.workload == "c4"
+                                       and world > 1 else
+                                       f"{world} rank(s), independent "
+                                       f"streams{wave_txt}")},
             "roofline": {"bound": "hbm",
-                         "kernel": "the frame step: fast_kernel (hot pass) + "
-                                   "deep_kernel (worklist + finalize), timed "
-                                   "together with CUDA events on the engine "
-                                   "stream; ncu share in profiles/",
-                         "achieved": achieved,
-                         "peak": peak * (world if args.workload == "c4" else 1),
+                         "kernel": "the fused frame step (fast_kernel + "
+                                   "deep_kernel), CUDA events on the engine "
+                                   "stream",
+                         "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / (peak * (world if args.workload
-                                                     == "c4" else 1)),
-                         "bytes_per_step": steps_bytes,
-                         "traffic": traffic},
+                         "frac": achieved / peak,
+                         "algorithmic_bytes_per_step": b_step,
+                         "traffic": traffic,
+                         "bytes_used": "min(algorithmic, traffic)"
+                                       if traffic else "algorithmic"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "pixel-frames/s",
-                    "h2d_bytes_per_step": int(bi),
-                    "d2h_bytes_per_step": int(bo)},
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk.summary(),
-            "extra": {"train_s": wl.t_train, "scene_gen_s": wl.t_gen,
-                      "warm_l2_ms_per_step": warm_ms,
-                      "step_ms_min": float(np.min(durs)),
-                      "step_ms_max": float(np.max(durs)),
+                    "h2d_bytes_per_step": int(bi // len(waves)),
+                    "d2h_bytes_per_step": int(bo // len(waves))},
+            "gpu_launches": 2 * args.steps * len(waves),
+            "clocks": clk.summary() if clk else None,
+            "extra": {"train_s": t_train, "scene_gen_s": t_gen,
+                      "step_ms_min": float(np.min(durs_all)),
+                      "step_ms_max": float(np.max(durs_all)),
                       "level_fractions": {k_: float(x) for k_, x in zip(
                           ("chp", "group", "mean", "meanvar", "gmm", "skip"),
                           lvl)}},
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
         if args.out:
             Path(args.out).write_text(json.dumps(line, indent=1))
     if world > 1:

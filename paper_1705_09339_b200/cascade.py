@@ -659,6 +659,11 @@ class CascadeEngine:
                 slot["cup"].handle,
                 slot["cdone"].handle)
             _lib.check(rc, "cog_step_host")
+            if src is frame:
+                # the caller owns this pinned buffer and may refill it as
+                # soon as we return (the reference reads its input
+                # synchronously): wait for the upload, not the step
+                slot["cup"].synchronize()
             self._advance()
             ev = slot["cdone"]
         else:
@@ -671,6 +676,8 @@ class CascadeEngine:
                 with torch.cuda.stream(ring.copy_stream):
                     x.copy_(src, non_blocking=True)
                     slot["up"].record(ring.copy_stream)
+                if src is frame:
+                    slot["up"].synchronize()   # caller-owned pinned input
                 compute.wait_event(slot["up"])
             self._launch_step(x, slot["mask"], slot["stats"])
             stepped = torch.cuda.Event()

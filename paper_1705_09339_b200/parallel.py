@@ -286,26 +286,29 @@ class BandSet:
 class BatchResult:
     """Masks (S, H, W) u8 and statistics rows (S, 10) i64 of one batch
     step, downloaded asynchronously into a pinned slot of the engine's ring;
-    ``masks`` / ``stats`` block on the download.  A slot is reused three
-    submissions later; a result still referring to it is copied out first,
-    so results stay valid however long they are kept."""
+    ``masks`` / ``stats`` block on the download.  The first read copies the
+    result out of the slot into arrays the result owns (the slot is reused
+    three submissions later), so arrays a caller already holds are never
+    overwritten by later frames."""
 
     def __init__(self, slot: dict) -> None:
         self._slot = slot
         self._own = None
 
     def _wait(self):
-        if self._own is not None:
-            return self._own
-        self._slot["down"].synchronize()
-        return (self._slot["hm"].numpy(), self._slot["hs"].numpy()[:, :10])
+        if self._own is None:
+            slot = self._slot
+            slot["down"].synchronize()
+            self._own = (slot["hm"].numpy().copy(),
+                         slot["hs"].numpy()[:, :10].copy())
+            if slot.get("owner") is self:
+                slot["owner"] = None
+            self._slot = None
+        return self._own
 
     def detach(self) -> None:
         """Copy out of the slot (called before the slot is reused)."""
-        if self._own is None:
-            m, st = self._wait()
-            self._own = (m.copy(), st.copy())
-        self._slot = None
+        self._wait()
 
     @property
     def masks(self) -> np.ndarray:
@@ -466,6 +469,8 @@ class BatchEngine:
                 self._copy.wait_event(slot["step"])  # device input reusable
             slot["x"].copy_(src, non_blocking=True)
             slot["up"].record(self._copy)
+        if src is frames:
+            slot["up"].synchronize()   # caller-owned pinned input: reusable
         compute.wait_event(slot["up"])
         self.process_frames_device(slot["x"], slot["m"], slot["s"])
         slot["step"].record(compute)

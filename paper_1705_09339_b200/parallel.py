@@ -358,6 +358,7 @@ class BatchEngine:
         proxy = CascadeEngine.__new__(CascadeEngine)  # param/geom carrier
         proxy.config, proxy.dev, proxy._wtab = config, eng.dev, eng._wtab
         proxy.exact_group_sums = False
+        proxy.kernel_variant = "auto"
         maps = []
         for s in range(S):
             arr = first if s == 0 else stack_training(frames_per_stream[s])

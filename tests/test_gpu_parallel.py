@@ -169,7 +169,7 @@ def test_many_groups_fall_back_to_a_kernel_that_fits():
     spec = synth.small_spec(2, 64, 48, 50, 30)
     frames = synth.Scene(spec).frames(0, 50)
     cfg = config_for({"k_max": 3, "color": True, "clusters": 400,
-                      "cluster_threshold": 3.0}, state_dtype="float32")
+                      "cluster_threshold": 1.0}, state_dtype="float32")
     eng = train_engine(frames[:30], cfg)
     assert eng.dev.n_groups > 160, eng.dev.n_groups
     ref = orc.train(frames[:30], cfg)

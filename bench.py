@@ -515,6 +515,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="minimum CPU time of the cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--variant", default="auto",
+                    help="step kernel (engine.kernel_variant; A/B tooling)")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -545,6 +547,7 @@ def main():
             del wl
             torch.cuda.empty_cache()
         wl = Workload(args.workload, args, world, rank, streams=wave)
+        wl.eng.kernel_variant = args.variant
         t_train += wl.t_train
         t_gen += wl.t_gen
         eng, cfg = wl.eng, wl.cfg

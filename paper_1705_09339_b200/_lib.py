@@ -44,13 +44,18 @@ def nvcc() -> str:
     return cand if Path(cand).exists() else "nvcc"
 
 
-def build_extension(force: bool = False, verbose: bool = False) -> Path:
-    """Compile libcog_b200.so in-tree if it is missing or stale."""
+def build_extension(force: bool = False, verbose: bool = False,
+                    defines: tuple = ()) -> Path:
+    """Compile libcog_b200.so in-tree if it is missing or stale.  `defines`
+    (NAME=VALUE build-time tuning macros, tools/ab_build.sh) force a
+    rebuild."""
     newest = max(p.stat().st_mtime for p in SOURCES + HEADERS)
-    if not force and SO_PATH.exists() and SO_PATH.stat().st_mtime >= newest:
+    if (not force and not defines and SO_PATH.exists()
+            and SO_PATH.stat().st_mtime >= newest):
         return SO_PATH
     tmp = SO_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp),
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines],
+           "-I", str(ROOT / "include"), "-o", str(tmp),
            *[str(s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -91,7 +96,7 @@ class Params(ctypes.Structure):
 
 
 # cog_params.variant: which step kernel (a parity knob; 0 = automatic)
-VARIANTS = {"auto": 0, "general": 1, "lean": 2}
+VARIANTS = {"auto": 0, "general": 1, "lean": 2, "tiles": 3}
 
 
 class State(ctypes.Structure):

@@ -46,6 +46,7 @@ struct FastConst {
   float ct_margin[3];  // |conf - ct| below this -> exact path, per class
   int eps_i;         // changed  <=>  |v - chp| > eps_i
   int sat;           // saturation_frames (clamped to int)
+  int big;           // hot_kernel: group sums / constants in global memory
 };
 
 FastConst make_fast_const(const cog_params& q) {

@@ -1,0 +1,517 @@
+// cog_hot.cuh -- the float32-state hot pass of the frame step (the
+// throughput path).  Included inside the anonymous namespace of
+// cog_kernels.cu, after cog_fast.cuh (FastConst, fmatch, the u16 prior).
+//
+// Work unit: one stride-aligned warp tile (stride rows x cw columns, so
+// every copy pixel's anchor is in row 0 of the same tile).  A CTA is D
+// warps; warp c runs plane c of the tile, one thread per plane-pixel (the
+// reference's planes are independent, cascade.py:281), and the planes meet
+// once per tile in shared memory for the union mask.  One thread therefore
+// holds one plane-pixel's state: no plane loop, no register rotation, no
+// spills, and ~60 warps per SM in flight.
+//
+// The hot loop has no calls and no binary64 fallback.  A plane-pixel whose
+// fp32 decision lies inside a filter margin (the u16 prior's quantisation
+// plus 1e-5 relative, see cog_fast.cuh) is DEFERRED: the hot pass writes
+// nothing for it and queues it on the stream's worklist, where deep_kernel
+// runs the general binary64 step (hot_px) for it.  MEANVAR hits and GMM
+// fall-throughs are queued as before.  A label that only becomes known in
+// the deep pass (GMM, deferred) is OR-ed into dyn and the mask there --
+// together with the labels of the copy pixels that read it
+// (kernels_numba.py:363-373): the queued item carries their positions.
+//
+// Loads per plane-pixel, in two dependent rounds: the frame byte, dyn,
+// meta, streak (+ the pixel's class and group id); then the hot prior
+// phat(v) from the u16 tile-major table and -- only when the cascade can
+// reach a mode level or the confidence reads a mode -- the (mu, var) pairs
+// of the two referenced modes, 8 bytes each from the 64-B record.
+
+constexpr int HQ_CAP = 64;  // per-warp worklist buffer (one global atomic per flush)
+
+// pending illumination reset / scheduled reorder of the plane-pixels this
+// thread evaluates (the CTA's tiles, plane c): out of line, called once per
+// frame, so the hot loop's registers never live across a call
+template <int KMAX>
+__device__ __noinline__ void hot_pending(const StepArgs* __restrict__ ap,
+                                         int s, int c, bool do_reset,
+                                         bool do_reorder) {
+  using T = float;
+  const StepArgs& a = *ap;
+  const int lane = threadIdx.x & 31;
+  const int H = a.g.height, W = a.g.width, stride = a.g.stride;
+  const int G = a.g.n_groups, D = a.g.depth;
+  const uint32_t P = (uint32_t)H * (uint32_t)W;
+  const int cw = a.cw;
+  const int lrow = lane / cw, lcol = lane - lrow * cw;
+  const bool lane_ok = lane < stride * cw;
+  const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+  const double* gmu = a.s.g_mu + ((size_t)s * D + c) * G;
+  for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+    const int ty = t / a.tiles_x, tx = t - ty * a.tiles_x;
+    const int y = ty * stride + lrow, x = tx * cw + lcol;
+    if (!(lane_ok && y < H && x < W)) continue;
+    const uint32_t p = (uint32_t)y * (uint32_t)W + (uint32_t)x;
+    if (do_reset) cold_reset<T, KMAX>(pr, p, a.q.initial_variance);
+    if (do_reorder) {
+      const int g0 = a.s.gid[(size_t)s * P + p];
+      cold_reorder<T>(pr, p, (G > 0 && g0 != (int)UNGROUPED)
+                                 ? gmu[g0] : (G > 0 ? gmu[0] : 0.0));
+    }
+  }
+}
+
+// shared memory of one CTA; `big`: the group sums and constants do not fit
+// (hundreds of groups) and live in global memory instead
+__host__ __device__ inline size_t hot_smem_bytes(int d, int G, bool big) {
+  const int g = big ? 0 : G;
+  const size_t wpad = ((size_t)acc_words(d, g) + 1) & ~(size_t)1;
+  return (size_t)d * wpad * 8 + (size_t)d * HQ_CAP * 16 +
+         (size_t)2 * d * g * 4 + (size_t)2 * d * 4 + 16;
+}
+
+// compile-time configuration of a hot_kernel instantiation: FL < 0 reads
+// the feature switches from the params, else bit 0 sampling, 1 grouping,
+// 2 change-hypothesis probe, 3 rate scaling, 4 literal confidence; ST = 0
+// reads the stride from the geometry
+enum : int { HF_SAMPLING = 1, HF_GROUPING = 2, HF_CHP = 4, HF_RATE = 8,
+             HF_LITERAL = 16 };
+constexpr int HF_DEFAULT = HF_SAMPLING | HF_GROUPING | HF_CHP | HF_RATE;
+
+#ifndef COG_HOT_MINB
+#define COG_HOT_MINB 30
+#endif
+
+template <int KMAX, int D, int ST, int FL>
+__global__ void __launch_bounds__(32 * D, COG_HOT_MINB / D)
+    hot_kernel(const __grid_constant__ StepArgs a,
+               const __grid_constant__ FastConst k) {
+  using T = float;
+  constexpr int R = rec_elems(KMAX), WO = rec_w(KMAX);
+  extern __shared__ unsigned long long h_mem[];
+  const int s = blockIdx.y;
+  const int G = a.g.n_groups;
+  const int H = a.g.height, W = a.g.width;
+  const int stride = ST > 0 ? ST : a.g.stride;
+  const int cw = ST > 0 ? ST * (32 / (ST * ST) > 0 ? 32 / (ST * ST) : 1) : a.cw;
+  const uint32_t P = (uint32_t)H * (uint32_t)W;
+  const int words = acc_words(D, G);
+  const bool big = k.big != 0;  // group sums / constants in global memory
+  const int sG = big ? 0 : G;
+  const int wpad = (acc_words(D, sG) + 1) & ~1;
+  const int lane = threadIdx.x & 31;
+  const int c = threadIdx.x >> 5;  // this warp's plane
+  const bool sampling = FL < 0 ? a.q.sampling_on != 0 : (FL & HF_SAMPLING) != 0;
+  const bool grouping = FL < 0 ? a.q.grouping_on != 0 : (FL & HF_GROUPING) != 0;
+  const bool chp_on = FL < 0 ? a.q.chp_on != 0 : (FL & HF_CHP) != 0;
+  const bool rate_on = FL < 0 ? a.q.rate_scaling_on != 0 : (FL & HF_RATE) != 0;
+  const bool literal = FL < 0 ? a.q.literal_conf != 0 : (FL & HF_LITERAL) != 0;
+
+  // ---- shared: warp-private partial slices (lane 0 adds, no atomics),
+  // per-warp worklist buffers, group constants (float), the tile's
+  // per-plane label words (double buffered)
+  unsigned long long* s_wacc = h_mem;                    // [D][wpad]
+  unsigned long long* s_qc = s_wacc + D * wpad;          // [D][HQ_CAP]
+  double* s_qr = (double*)(s_qc + D * HQ_CAP);           // [D][HQ_CAP]
+  float* s_gmu = (float*)(s_qr + D * HQ_CAP);            // [D*G]
+  float* s_gthr = s_gmu + D * sG;                        // [D*G]
+  unsigned* s_lab = (unsigned*)(s_gthr + D * sG);        // [2][D]
+  const double* gmu_d = a.s.g_mu + (size_t)s * D * G;
+  const double* gvar_d = a.s.g_var + (size_t)s * D * G;
+  for (int i = threadIdx.x; i < D * sG; i += 32 * D) {
+    s_gmu[i] = (float)gmu_d[i];
+    s_gthr[i] = (float)(a.q.match_lambda * sqrt(gvar_d[i]));
+  }
+  for (int i = threadIdx.x; i < D * wpad; i += 32 * D) s_wacc[i] = 0ull;
+  __syncthreads();
+  // let the frame's deep kernel be scheduled now (it waits on this grid's
+  // completion before touching anything); hides the launch gap
+  asm volatile("griddepcontrol.launch_dependents;");
+  unsigned long long* const wacc = s_wacc + c * wpad;
+  unsigned long long* const qc = s_qc + c * HQ_CAP;
+  double* const qr = s_qr + c * HQ_CAP;
+
+  // 32-bit element indices from the state arrays' own bases (the launcher
+  // guarantees streams * d * 5 * P and the record elements < 2^32)
+  const uint32_t s1 = (uint32_t)s * P;                  // [s][P] arrays
+  const uint32_t plane = ((uint32_t)s * D + c) * P;     // [s][d][P] arrays
+  T* const mix_s = (T*)a.s.mix;
+  T* const conf_s = (T*)a.conf;
+  unsigned long long* const gacc =
+      (unsigned long long*)a.s.accum + (size_t)s * words;
+  uint32_t* const sync = a.s.sync + (size_t)s * 4;
+  const size_t dq_cap = dq_capacity(D, P);
+  unsigned long long* const dq_code =
+      (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
+  double* const dq_rho = a.s.deeprho + (size_t)s * dq_cap;
+  const bool do_reset = (*(volatile uint32_t*)(sync + 1) & 1u) != 0;
+  const bool do_reorder = a.reorder_now != 0;
+  // this warp's plane of the hot prior: tile t, bin v, slot at
+  // (t * 256 + v) * 32 + slot
+  const uint16_t* const tq =
+      a.s.tabq + ((size_t)s * D + c) * (size_t)a.n_tiles * 8192 + lane;
+
+  const int lrow = lane / cw, lcol = lane - lrow * cw;
+  const bool lane_ok = lane < stride * cw;
+  const bool on_lat = (lrow == 0) && (lcol % stride == 0);
+  const int anchor = lcol - lcol % stride;
+
+  // ---- a pending illumination reset / scheduled reorder (rare, uniform
+  // over the grid): applied per plane-pixel before the frame's own pass,
+  // over the same tiles this thread evaluates below
+  if (do_reset || do_reorder) hot_pending<KMAX>(&a, s, c, do_reset, do_reorder);
+
+  unsigned long long kc = 0ull;  // kind counts, 7 x 9 bits
+  int kc_units = 0;
+  int wq_n = 0;
+  unsigned fg_count = 0;
+  int it = 0;
+  // tile t = ty * tiles_x + tx, advanced by the grid size without a division
+  const int dty = gridDim.x / a.tiles_x, dtx = gridDim.x - dty * a.tiles_x;
+  int ty = blockIdx.x / a.tiles_x, tx = blockIdx.x - ty * a.tiles_x;
+  for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++it) {
+    const int y = ty * stride + lrow, x = tx * cw + lcol;
+    ty += dty;
+    tx += dtx;
+    if (tx >= a.tiles_x) {
+      tx -= a.tiles_x;
+      ty += 1;
+    }
+    const bool valid = lane_ok && y < H && x < W;
+    const uint32_t p = valid ? (uint32_t)y * (uint32_t)W + (uint32_t)x : 0u;
+    const uint32_t o = plane + p;
+
+    // ---- round 1 (addresses are in range for every lane; invalid lanes
+    // read pixel 0 and write nothing)
+    const int vb = a.frame[o];
+    const uint32_t dyn = a.s.dyn[o];
+    const uint32_t meta = a.s.meta[o];
+    const uint32_t sk = a.s.streak[o];
+    const int gid = a.s.gid[s1 + p];
+    const int cls = a.s.cls[s1 + p];
+    const bool member = valid && G > 0 && gid != (int)UNGROUPED;
+    const int gidx = member ? c * G + gid : 0;
+    const int dv = abs(vb - (int)(dyn & 0xFF));
+    const bool changed = dv > k.eps_i;
+    const int last_label = (dyn >> 8) & 1u;
+
+    // ---- sampling gate (kernels_numba.py:189-216): skip, copy, evaluate
+    // (after waking on a change the streak restarts)
+    const bool asleep = sampling && (dyn >> 16) != 0u;
+    const bool waking = sampling && !asleep && ((dyn >> 9) & 1u);
+    const bool skip = asleep && !changed;
+    const bool copy = waking && !changed && !on_lat;
+    const bool ev = valid && !skip && !copy;
+
+    // ---- level codes, the group test from shared memory, round 2
+    const uint32_t c0 = (meta >> 4) & 3u, c1 = (meta >> 6) & 3u,
+                   c2 = (meta >> 8) & 3u;
+    const uint32_t r0 = (meta >> 10) & 7u, r1 = meta >> 13;
+    const uint32_t top = (c0 == L_GROUP && !grouping) ? c1 : c0;
+    const bool gtop = top == L_GROUP && member;
+    const float vf = (float)vb;
+    float gm = 0.0f, gthr = 1.0f;
+    if (member) {
+      if (!big) {
+        gm = s_gmu[gidx];
+        gthr = s_gthr[gidx];
+      } else {
+        gm = (float)gmu_d[gidx];
+        gthr = (float)(a.q.match_lambda * sqrt(gvar_d[gidx]));
+      }
+    }
+    const int ghit = (grouping && member) ? fmatch(vf, gm, gthr) : 0;
+    const bool chp_hit = chp_on && !changed;
+    // the modes are needed unless the confidence reads the group and the
+    // walk stops at the group level (or the probe) before any mode level
+    const bool need =
+        ev && !(gtop && (chp_hit || (c0 == L_GROUP && ghit == 1)));
+    T* const rec = mix_s + o * R;  // this plane-pixel's mixture record
+    uint32_t q16 = 0u;
+    float2 m0 = make_float2(0.0f, 1.0f), m1 = m0;
+    if (ev) q16 = __ldcg(tq + ((size_t)t * 256 + vb) * 32);
+    if (need) {
+      m0 = *reinterpret_cast<const float2*>(rec + 2 * r0);
+      m1 = *reinterpret_cast<const float2*>(rec + 2 * r1);
+    }
+
+    // ---- evaluation (kernels_numba.py:239-359) in fp32; a decision whose
+    // fp32 operands lie inside the filter margin defers the plane-pixel
+    const float thr0 = k.lam * (m0.y * rsqrt_approx(m0.y));
+    const float thr1 = k.lam * (m1.y * rsqrt_approx(m1.y));
+    const float wa = cls == 0 ? k.w[0] : (cls == 1 ? k.w[3] : k.w[6]);
+    const float wb = cls == 0 ? k.w[1] : (cls == 1 ? k.w[4] : k.w[7]);
+    const float wc = cls == 0 ? k.w[2] : (cls == 1 ? k.w[5] : k.w[8]);
+    const bool top1 = top == L_MEANVAR;
+    const float mt = gtop ? gm : (top1 ? m1.x : m0.x);
+    const float dn = gtop ? gthr : (top1 ? thr1 : thr0);
+    const float ph = (float)q16 * PH_Q;
+    const float btl = (float)dv * (1.0f / 255.0f);
+    const float bt = literal ? btl : 1.0f - btl;
+    const float gtl = fminf(fabsf(vf - mt) * rcp_approx(dn), 1.0f);
+    const float gt = literal ? gtl : 1.0f - gtl;
+    const float wbc = __fmaf_rn(wb, bt, __fmul_rn(wc, gt));
+    const bool floor_ = ph < k.pf;
+    const float wbci =
+        cls == 0 ? k.wbc_inv[0] : (cls == 1 ? k.wbc_inv[1] : k.wbc_inv[2]);
+    const float cf_ev = floor_ ? __fmul_rn(wbc, wbci) : __fmaf_rn(wa, ph, wbc);
+    const float ct_m = cls == 0 ? k.ct_margin[0]
+                                : (cls == 1 ? k.ct_margin[1] : k.ct_margin[2]);
+    bool deferred = ev && (fabsf(ph - k.pf) <= k.pf_margin ||
+                           fabsf(cf_ev - k.ct) <= ct_m);
+    // the level tests, then the first hit in mid_order (the first test
+    // that is not a miss decides; an undecided one defers)
+    int hm0 = fmatch(vf, m0.x, thr0), hm1 = fmatch(vf, m1.x, thr1);
+    auto walk = [&]() {
+      int act = L_GMM;
+#pragma unroll
+      for (int j = 2; j >= 0; --j) {  // the earliest decisive test wins
+        const uint32_t code = j == 0 ? c0 : (j == 1 ? c1 : c2);
+        if (code == 0) {
+          act = L_GMM;  // the walk ends before this code
+          continue;
+        }
+        const int hit = code == L_GROUP ? ghit : (code == L_MEAN ? hm0 : hm1);
+        if (hit != 0) act = hit > 0 ? (int)code : -1;
+      }
+      return act;
+    };
+    int active = L_CHP, label = chp_hit ? last_label : 0;
+    if (!chp_hit) {
+      active = walk();
+      // a matched mode must also sit inside the background weight prefix,
+      // else the walk continues (kernels_numba.py:298-311); rare: only
+      // when the matched mode is not the first one
+      for (int guard = 0; guard < 2 && ev; ++guard) {
+        const bool m = active == L_MEAN && r0 > 0;
+        const bool mv = active == L_MEANVAR && r1 > 0;
+        if (!m && !mv) break;
+        const uint32_t rr = m ? r0 : r1;
+        double acc = 0.0;
+        for (uint32_t q = 0; q < rr; ++q) acc = acc + (double)rec[WO + q];
+        if (acc <= a.q.background_threshold) break;
+        if (m) hm0 = 0;
+        else hm1 = 0;
+        active = walk();
+      }
+    }
+    if (active < 0) {
+      deferred |= ev;
+      active = L_GMM;
+    }
+    const bool fast = ev && !deferred;
+    const int deep = !fast ? DEEP_NONE
+                           : (active == L_MEANVAR ? DEEP_MEANVAR
+                                                  : (active == L_GMM ? DEEP_GMM
+                                                                     : DEEP_NONE));
+    double rho = a.q.learning_rate;
+    if (rate_on) {
+      double relax = 1.0 - (double)cf_ev;
+      if (relax < a.q.rate_floor) relax = a.q.rate_floor;
+      rho = a.q.learning_rate * relax;
+    }
+    const uint32_t la_bits = dyn & (7u << 10);  // last_active + 1, kept
+    int kind;
+    uint32_t dyn_out;
+    float cf = 0.0f;
+    if (skip) {
+      // asleep and unchanged (kernels_numba.py:194-203)
+      const uint32_t clk = (dyn >> 16) - 1u;
+      kind = K_SKIP;
+      label = last_label;
+      dyn_out = (uint32_t)vb | ((uint32_t)last_label << 8) |
+                (((uint32_t)(clk == 0u) | ((dyn >> 9) & 1u)) << 9) | la_bits |
+                (clk << 16);
+    } else if (copy) {
+      // waking, unchanged, off the lattice (kernels_numba.py:207-216)
+      kind = K_COPY;
+      label = 0;
+      dyn_out = (uint32_t)vb | la_bits | ((uint32_t)a.q.sleep_frames << 16);
+    } else {
+      // ---- bookkeeping (kernels_numba.py:335-359)
+      kind = active;
+      cf = cf_ev;
+      const uint32_t skn0 = (asleep || !fast) ? 0u : sk;  // woke: restart
+      const uint32_t skn =
+          cf_ev > k.ct ? (skn0 == 0xffffffffu ? skn0 : skn0 + 1u) : 0u;
+      uint32_t clock = 0u, wk = 0u;
+      if (!sampling) {
+        clock = dyn >> 16;
+        wk = (dyn >> 9) & 1u;
+      } else if ((long long)skn >= (long long)k.sat) {
+        clock = (uint32_t)a.q.sleep_frames;
+      }
+      dyn_out = (uint32_t)vb | ((uint32_t)label << 8) | (wk << 9) |
+                ((uint32_t)(active + 1) << 10) | (clock << 16);
+      if (fast) {
+        a.s.streak[o] = skn;
+        atomicAdd(a.s.hits + (plane * 5 + (uint32_t)active * P + p), 1u);
+        if (active == L_MEAN)
+          rec[2 * r0] = (float)((1.0 - rho) * (double)m0.x + rho * (double)vb);
+      }
+    }
+
+    // ---- copies take the anchor's label when it is known now; a label
+    // that arrives with the deep pass (GMM, deferred) is written there,
+    // for the anchor and its copies
+    const bool late = deferred || deep == DEEP_GMM;
+    const int now = late ? 0 : label;
+    const int al = __shfl_sync(FULL, now, anchor);
+    const bool is_copy = valid && copy;
+    const int lab_now = is_copy ? al : now;
+    if (valid && !deferred)
+      a.s.dyn[o] = dyn_out | ((uint32_t)(is_copy ? al : (deep == DEEP_GMM ? 0 : label)) << 8);
+    const unsigned cm = __ballot_sync(FULL, is_copy);
+
+    // ---- worklist: MEANVAR hits, GMM fall-throughs, deferred plane-pixels
+    const bool item = valid && (deferred || deep != DEEP_NONE);
+    const unsigned qm = __ballot_sync(FULL, item);
+    if (qm) {
+      const int nq = __popc(qm);
+      if (wq_n + nq > HQ_CAP) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(sync + 3, (unsigned)wq_n);
+        base = __shfl_sync(FULL, base, 0);
+        __syncwarp();
+        for (int e = lane; e < wq_n; e += 32) {
+          dq_code[(size_t)base + e] = qc[e];
+          dq_rho[(size_t)base + e] = qr[e];
+        }
+        __syncwarp();
+        wq_n = 0;
+      }
+      if (item) {
+        unsigned cmk = 0;
+        if (late && on_lat && cm) {
+          // the copies of this anchor: lanes (r, anchor + dc) of the tile
+          int b = 0;
+          for (int r = 0; r < stride; ++r)
+            for (int dc = 0; dc < stride; ++dc) {
+              if (r == 0 && dc == 0) continue;
+              if ((cm >> (r * cw + lcol + dc)) & 1u) cmk |= 1u << b;
+              ++b;
+            }
+        }
+        const int pos = wq_n + __popc(qm & ((1u << lane) - 1u));
+        qc[pos] = 1ull | ((unsigned long long)deep << 1) |
+                  ((unsigned long long)(deep == DEEP_MEANVAR ? r1 : 0u) << 3) |
+                  ((unsigned long long)c << 6) |
+                  ((unsigned long long)vb << 8) |
+                  ((unsigned long long)p << 16) |
+                  ((unsigned long long)cmk << ITEM_COPY_SHIFT) |
+                  (deferred ? ITEM_DEFERRED : 0ull);
+        qr[pos] = rho;
+      }
+      wq_n += nq;
+    }
+
+    // ---- outputs, kind counts
+    if (valid && !deferred) {
+      conf_s[o] = cf;
+      a.kind[o] = (uint8_t)kind;
+      kc += 1ull << (9 * kind);
+    }
+
+    // ---- group partials (exact sums) into the warp's private slice, or
+    // straight into the stream's sums when they live in global memory
+    const unsigned any_member = __ballot_sync(FULL, member);
+    if (any_member) {
+      unsigned todo = any_member;
+      while (todo) {
+        const int leader = __ffs(todo) - 1;
+        const int g = __shfl_sync(FULL, gid, leader);
+        const bool mine = member && gid == g;
+        const unsigned mm = __ballot_sync(FULL, mine);
+        todo &= ~mm;
+        const unsigned sall = warp_sum_u32(mine ? (unsigned)vb : 0u);
+        const bool hit = mine && !deferred && kind == L_GROUP;
+        const unsigned hm = __ballot_sync(FULL, hit);
+        unsigned sv = 0, qh = 0, ql = 0;
+        if (hm) {
+          unsigned long long qv = 0;
+          if (hit) {
+            const double cq = (double)cf * 4503599627370496.0;  // 2^52
+            qv = cq > 0.0 ? (unsigned long long)cq : 0ull;
+          }
+          sv = warp_sum_u32(hit ? (unsigned)vb : 0u);
+          qh = warp_sum_u32((unsigned)(qv >> CONF_SPLIT));
+          ql = warp_sum_u32((unsigned)(qv & ((1ull << CONF_SPLIT) - 1ull)));
+        }
+        if (lane == 0) {
+          if (!big) {
+            unsigned long long* e = wacc + acc_grp(D, G, c, g);
+            e[4] += sall;
+            e[5] += (unsigned long long)__popc(mm);
+            if (hm) {
+              e[0] += (unsigned long long)__popc(hm);
+              e[1] += sv;
+              e[2] += qh;
+              e[3] += ql;
+            }
+          } else {
+            unsigned long long* e = gacc + acc_grp(D, G, c, g);
+            atomicAdd(e + 4, (unsigned long long)sall);
+            atomicAdd(e + 5, (unsigned long long)__popc(mm));
+            if (hm) {
+              atomicAdd(e + 0, (unsigned long long)__popc(hm));
+              atomicAdd(e + 1, (unsigned long long)sv);
+              atomicAdd(e + 2, (unsigned long long)qh);
+              atomicAdd(e + 3, (unsigned long long)ql);
+            }
+          }
+        }
+      }
+    }
+    if (++kc_units >= 511) {
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        const unsigned v = warp_sum_u32((unsigned)((kc >> (9 * q)) & 511u));
+        if (lane == 0) wacc[acc_kind(0, q)] += v;
+      }
+      kc = 0ull;
+      kc_units = 0;
+    }
+
+    // ---- union mask of the tile (labels known now; late ones are OR-ed
+    // in by the deep pass)
+    const unsigned lb = __ballot_sync(FULL, valid && lab_now != 0);
+    if (D == 1) {
+      if (valid) a.mask[s1 + p] = (lb >> lane) & 1u ? 255 : 0;
+      fg_count += __popc(lb);
+    } else {
+      unsigned* slot = s_lab + (it & 1) * D;
+      if (lane == 0) slot[c] = lb;
+      __syncthreads();
+      if (c == 0) {
+        unsigned u = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) u |= slot[j];
+        if (valid) a.mask[s1 + p] = (u >> lane) & 1u ? 255 : 0;
+        fg_count += __popc(u & __ballot_sync(FULL, valid));
+      }
+    }
+  }
+  if (wq_n) {
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(sync + 3, (unsigned)wq_n);
+    base = __shfl_sync(FULL, base, 0);
+    __syncwarp();
+    for (int e = lane; e < wq_n; e += 32) {
+      dq_code[(size_t)base + e] = qc[e];
+      dq_rho[(size_t)base + e] = qr[e];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    const unsigned v = warp_sum_u32((unsigned)((kc >> (9 * q)) & 511u));
+    if (lane == 0) wacc[acc_kind(0, q)] += v;
+  }
+  if (lane == 0) wacc[acc_fg(D)] += fg_count;
+  __syncthreads();
+  const int sw = acc_words(D, sG);  // words held in shared
+  for (int i = threadIdx.x; i < sw; i += 32 * D) {
+    unsigned long long v = 0;
+#pragma unroll
+    for (int w = 0; w < D; ++w) v += s_wacc[w * wpad + i];
+    if (v) atomicAdd(gacc + i, v);
+  }
+}

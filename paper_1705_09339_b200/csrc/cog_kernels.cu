@@ -756,6 +756,18 @@ __host__ __device__ inline size_t dq_capacity(int d, size_t P) {
   return (size_t)d * P;
 }
 
+// bterm tables |v - prev| / 255 (literal) and 1 - that (reference form,
+// kernels_numba.py:255-257), computed once on the host in IEEE binary64
+// (correctly rounded, as the device division) and uploaded per device, so
+// no CTA spends its prologue on 256 binary64 divisions
+__device__ double g_bterm[2][256];
+
+// worklist item code (u64): valid | deep << 1 | rsel << 3 | plane << 6 |
+// v << 8 | p << 16 (32 bits) | copy mask << 48 (15 bits) | deferred << 63;
+// the copy mask and the deferred flag come from the float32 hot pass only
+constexpr int ITEM_COPY_SHIFT = 48;
+constexpr unsigned long long ITEM_DEFERRED = 1ull << 63;
+
 constexpr int WQ_CAP = 128;  // warp-private worklist buffer (flushed when full)
 
 struct WarpScratch {  // one per warp, in dynamic shared memory
@@ -1250,6 +1262,37 @@ __global__ void __launch_bounds__(STEP_THREADS, COG_STEP_MINB)
 // mode references remapped.  A GMM label sets the label bit in dyn and --
 // unless the mask is formed by a union pass -- ORs the pixel's mask byte;
 // returns 1 iff that byte went 0 -> 255 (counted once per pixel).
+// A label that only becomes known in the deep pass (GMM fall-through,
+// deferred plane-pixel): the label bit of dyn and the mask byte of pixel p
+// and of the copy pixels that read their label from it (cmask: bit b is the
+// pixel b + 1 of the anchor's stride x stride block in row-major order,
+// kernels_numba.py:363-373).  Returns how many mask bytes went 0 -> 255.
+__device__ __forceinline__ unsigned or_mask_byte(uint8_t* m) {
+  const uintptr_t addr = (uintptr_t)m;
+  unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
+  const unsigned sh = (unsigned)(addr & 3) * 8;
+  const unsigned old = atomicOr(word, 0xFFu << sh);
+  return ((old >> sh) & 0xFFu) == 0u;
+}
+
+__device__ __noinline__ unsigned late_label(const StepArgs& a, int s, int c,
+                                            size_t p, unsigned cmask) {
+  const size_t P = (size_t)a.g.height * a.g.width;
+  uint32_t* dyn = a.s.dyn + ((size_t)s * a.g.depth + c) * P;
+  uint8_t* mask = a.mask + (size_t)s * P;
+  dyn[p] |= 1u << 8;
+  unsigned newly = or_mask_byte(mask + p);
+  const int st = a.g.stride;
+  for (int b = 0; cmask; ++b, cmask >>= 1) {
+    if (!(cmask & 1u)) continue;
+    const int idx = b + 1, r = idx / st, dc = idx - r * st;
+    const size_t q = p + (size_t)r * a.g.width + dc;
+    dyn[q] |= 1u << 8;
+    newly += or_mask_byte(mask + q);
+  }
+  return newly;
+}
+
 template <typename T, int KMAX>
 __device__ __forceinline__ unsigned deep_item(const StepArgs& a, int s,
                                               unsigned long long code,
@@ -1257,11 +1300,10 @@ __device__ __forceinline__ unsigned deep_item(const StepArgs& a, int s,
   const size_t P = (size_t)a.g.height * a.g.width;
   const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
                   a.q.variance_floor, a.q.initial_variance};
-  uint8_t* mask = a.mask + (size_t)s * P;
   const int kindq = (int)((code >> 1) & 3), rs = (int)((code >> 3) & 7);
   const int c = (int)((code >> 6) & 3);
   const double v = (double)((code >> 8) & 0xFF);
-  const size_t p = (size_t)(code >> 16);
+  const size_t p = (size_t)((code >> 16) & 0xFFFFFFFFull);
   const PlaneRef<T> pr = plane_ref<T>(a, s, c);
   // meta and the whole mixture record in one round of loads
   const uint32_t meta = pr.meta[p];
@@ -1296,14 +1338,7 @@ __device__ __forceinline__ unsigned deep_item(const StepArgs& a, int s,
       nm = meta_with_refs(nm, select_inv<KMAX>(inv, meta_ref(meta, 0)),
                           select_inv<KMAX>(inv, meta_ref(meta, 1)));
     pr.meta[p] = (uint16_t)nm;
-    if (lbl) {
-      pr.dyn[p] |= 1u << 8;
-      const uintptr_t addr = (uintptr_t)(mask + p);
-      unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
-      const unsigned sh = (unsigned)(addr & 3) * 8;
-      const unsigned old = atomicOr(word, 0xFFu << sh);
-      newly = ((old >> sh) & 0xFFu) == 0u;
-    }
+    if (lbl) newly = late_label(a, s, c, p, (unsigned)(code >> 48) & 0x7FFFu);
   }
   return newly;
 }
@@ -1393,7 +1428,7 @@ __device__ __forceinline__ unsigned deep_item_f32(const StepArgs& a, int s,
   const int kindq = (int)((code >> 1) & 3), rs = (int)((code >> 3) & 7);
   const int c = (int)((code >> 6) & 3);
   const float v = (float)((code >> 8) & 0xFF);
-  const size_t p = (size_t)(code >> 16);
+  const size_t p = (size_t)((code >> 16) & 0xFFFFFFFFull);
   const PlaneRef<float> pr = plane_ref<float>(a, s, c);
   const uint32_t meta = pr.meta[p];
   constexpr int R = rec_elems(KMAX), WO = rec_w(KMAX);
@@ -1532,16 +1567,97 @@ __device__ __forceinline__ unsigned deep_item_f32(const StepArgs& a, int s,
                         select_inv<KMAX>(inv, meta_ref(meta, 1)));
   pr.meta[p] = (uint16_t)nm;
   unsigned newly = 0;
-  if (label) {
-    pr.dyn[p] |= 1u << 8;
-    uint8_t* mask = a.mask + (size_t)s * P;
-    const uintptr_t addr = (uintptr_t)(mask + p);
-    unsigned* word = (unsigned*)(addr & ~(uintptr_t)3);
-    const unsigned sh = (unsigned)(addr & 3) * 8;
-    const unsigned old = atomicOr(word, 0xFFu << sh);
-    newly = ((old >> sh) & 0xFFu) == 0u;
-  }
+  if (label) newly = late_label(a, s, c, p, (unsigned)(code >> 48) & 0x7FFFu);
   return newly;
+}
+
+// A plane-pixel the float32 hot pass deferred (an fp32 decision inside its
+// filter margin): the general binary64 step of kernels_numba.py:188-359
+// (hot_px) from its untouched state, with the exact f32 table entry, then
+// everything the hot pass would have done for it -- confidence / kind
+// outputs, its kind count and group partials (into the stream's summed
+// partials, before the frame tail reads them), the deep update, and its
+// label (with its copies').  Returns the mask bytes that went 0 -> 255.
+template <int KMAX>
+__device__ __noinline__ unsigned deferred_item(const StepArgs& a, int s,
+                                               unsigned long long code,
+                                               unsigned long long* gacc) {
+  using T = float;
+  const int D = a.g.depth, G = a.g.n_groups;
+  const size_t P = (size_t)a.g.height * a.g.width;
+  const int c = (int)((code >> 6) & 3);
+  const int vb = (int)((code >> 8) & 0xFF);
+  const size_t p = (size_t)((code >> 16) & 0xFFFFFFFFull);
+  const unsigned cmask = (unsigned)(code >> 48) & 0x7FFFu;
+  const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+  const Flags f{a.q.sampling_on != 0, a.q.grouping_on != 0,
+                a.q.rate_scaling_on != 0, a.q.chp_on != 0,
+                a.q.literal_conf != 0, a.q.compat != 0};
+  Pre<T> x;
+  x.vb = vb;
+  x.dyn = pr.dyn[p];
+  x.meta = pr.meta[p];
+  x.streak = pr.streak[p];
+  x.tv = __ldcg(pr.table + p * 256 + vb);
+  x.peak = pr.peak[p];
+  {
+    const T* rec = rec_of(pr, p);
+    const int r0 = meta_ref(x.meta, 0), r1 = meta_ref(x.meta, 1);
+    x.mu0 = rec[2 * r0];
+    x.var0 = rec[2 * r0 + 1];
+    x.mu1 = rec[2 * r1];
+    x.var1 = rec[2 * r1 + 1];
+  }
+  const int W = a.g.width, st = a.g.stride;
+  const int y = (int)(p / (size_t)W), xx = (int)(p - (size_t)y * W);
+  const bool on_lat = ((a.g.row0 + y) % st == 0) && (xx % st == 0);
+  const int cls = a.s.cls[(size_t)s * P + p];
+  const int gid = a.s.gid[(size_t)s * P + p];
+  const bool member = G > 0 && gid != (int)UNGROUPED;
+  GroupConst gc;
+  gc.ok = member;
+  gc.mu = 0.0;
+  gc.thr = 0.0;
+  if (member) {
+    const size_t gi = ((size_t)s * D + c) * G + gid;
+    gc.mu = a.s.g_mu[gi];
+    gc.thr = a.q.match_lambda * sqrt(a.s.g_var[gi]);
+  }
+  HotOut h;
+  h.kind = 0;
+  h.label = 0;
+  h.deep = DEEP_NONE;
+  h.conf = 0.0;
+  h.rho = 0.0;
+  h.rsel = 0;
+  h.dyn = 0;
+  hot_px<T>(a, f, pr, p, x, on_lat, g_bterm[f.literal ? 1 : 0],
+            a.q.weights[3 * cls], a.q.weights[3 * cls + 1],
+            a.q.weights[3 * cls + 2], gc, h);
+  const size_t o = ((size_t)s * D + c) * P + p;
+  ((T*)a.conf)[o] = (T)h.conf;
+  a.kind[o] = (uint8_t)h.kind;
+  atomicAdd(gacc + acc_kind(0, h.kind), 1ull);
+  if (member && h.kind == L_GROUP) {
+    unsigned long long* e = gacc + acc_grp(D, G, c, gid);
+    const double cq = h.conf * 4503599627370496.0;  // 2^52
+    const unsigned long long qv = cq > 0.0 ? (unsigned long long)cq : 0ull;
+    atomicAdd(e + 0, 1ull);
+    atomicAdd(e + 1, (unsigned long long)vb);
+    atomicAdd(e + 2, qv >> CONF_SPLIT);
+    atomicAdd(e + 3, qv & ((1ull << CONF_SPLIT) - 1ull));
+  }
+  int label = h.label;
+  if (h.deep == DEEP_MEANVAR) {
+    cold_meanvar<T, KMAX>(pr, p, x.meta, h.rsel, (double)vb, h.rho,
+                          a.q.variance_floor);
+  } else if (h.deep == DEEP_GMM) {
+    const GmmPar gp{a.q.match_lambda, a.q.background_threshold,
+                    a.q.variance_floor, a.q.initial_variance};
+    label = cold_gmm<T, KMAX>(pr, p, x.meta, (double)vb, h.rho, gp, a.g.k, 1);
+    pr.dyn[p] = h.dyn;
+  }
+  return label ? late_label(a, s, c, p, cmask) : 0u;
 }
 
 template <typename T, int KMAX>
@@ -1562,6 +1678,9 @@ __global__ void __launch_bounds__(DEEP_THREADS) deep_kernel(const StepArgs a) {
   if (threadIdx.x == 0) s_fg = 0;
   __syncthreads();
   unsigned fg = 0;
+  const int words = acc_words(d, a.g.n_groups);
+  unsigned long long* gacc =
+      (unsigned long long*)a.s.accum + (size_t)s * words;
   // warp-granular round robin over the CTAs (warp 0 of every CTA first):
   // a short worklist spreads over all SMs instead of filling the first
   // few CTAs
@@ -1573,6 +1692,10 @@ __global__ void __launch_bounds__(DEEP_THREADS) deep_kernel(const StepArgs a) {
     if (!(code & 1ull)) continue;
     dq_code[i] = 0ull;
     if constexpr (sizeof(T) == 4) {
+      if (code & ITEM_DEFERRED) {
+        fg += deferred_item<KMAX>(a, s, code, gacc);
+        continue;
+      }
       if (!a.q.compat) {  // fp32 arithmetic, binary64 fallback near ties
         bool ok;
         const unsigned nw = deep_item_f32<KMAX>(a, s, code, dq_rho[i], ok);
@@ -1587,9 +1710,6 @@ __global__ void __launch_bounds__(DEEP_THREADS) deep_kernel(const StepArgs a) {
   for (int o = 16; o > 0; o >>= 1) fg += __shfl_xor_sync(FULL, fg, o);
   if ((threadIdx.x & 31) == 0 && fg) atomicAdd(&s_fg, (unsigned long long)fg);
   __syncthreads();
-  const int words = acc_words(d, a.g.n_groups);
-  unsigned long long* gacc =
-      (unsigned long long*)a.s.accum + (size_t)s * words;
   if (threadIdx.x == 0 && s_fg) atomicAdd(gacc + acc_fg(d), s_fg);
   if (!a.fuse_finalize) return;
   __threadfence();
@@ -2003,14 +2123,9 @@ __global__ void import_kernel(cog_geom g, cog_state s, cog_ref_state in) {
   }
 }
 
-// bterm tables |v - prev| / 255 (literal) and 1 - that (reference form,
-// kernels_numba.py:255-257), computed once on the host in IEEE binary64
-// (correctly rounded, as the device division) and uploaded per device, so
-// no CTA spends its prologue on 256 binary64 divisions
-__device__ double g_bterm[2][256];
-
 #include "cog_lean.cuh"
 #include "cog_fast.cuh"
+#include "cog_hot.cuh"
 
 // ---------------------------------------------------------------------------
 // training: k-means assignment step (grouping.py:116-118): squared distance
@@ -2324,6 +2439,55 @@ int launch_fast(const StepArgs& a, cudaStream_t st) {
   return launch_fast_k<8, 3>(a, st);
 }
 
+template <int KMAX, int D, int ST, int FL>
+int launch_hot_k(const StepArgs& a, cudaStream_t st) {
+  auto fn = hot_kernel<KMAX, D, ST, FL>;
+  // the group sums and constants move to global memory when they would
+  // not fit comfortably (hundreds of groups): any group count runs
+  const bool big = hot_smem_bytes(a.g.depth, a.g.n_groups, false) > 24 * 1024;
+  const size_t smem = hot_smem_bytes(a.g.depth, a.g.n_groups, big);
+  if (smem > SMEM_CAP) return COG_EUNSUPPORTED;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  const int threads = 32 * D;
+  const int occ = cached_occupancy((const void*)fn, threads, smem);
+  // one tile per CTA at a time, CTAs striding over the tiles; every CTA of
+  // every stream resident in one wave
+  int per_stream = (num_sms() * occ) / a.g.streams;
+  if (per_stream < 1) per_stream = 1;
+  const int gx = a.n_tiles < per_stream ? a.n_tiles : per_stream;
+  FastConst k = make_fast_const(a.q);
+  k.big = big ? 1 : 0;
+  fn<<<dim3(gx < 1 ? 1 : gx, a.g.streams), threads, smem, st>>>(a, k);
+  return launch_status();
+}
+
+// the production configuration (stride 2, the reference's default feature
+// switches) is compiled in; anything else reads them at run time
+template <int KMAX, int D>
+int launch_hot_cfg(const StepArgs& a, cudaStream_t st) {
+  const int fl = (a.q.sampling_on ? HF_SAMPLING : 0) |
+                 (a.q.grouping_on ? HF_GROUPING : 0) |
+                 (a.q.chp_on ? HF_CHP : 0) |
+                 (a.q.rate_scaling_on ? HF_RATE : 0) |
+                 (a.q.literal_conf ? HF_LITERAL : 0);
+  if (a.g.stride == 2 && fl == HF_DEFAULT)
+    return launch_hot_k<KMAX, D, 2, HF_DEFAULT>(a, st);
+  return launch_hot_k<KMAX, D, 0, -1>(a, st);
+}
+
+int launch_hotpass(const StepArgs& a, cudaStream_t st) {
+  if (a.g.depth == 1) {
+    if (a.g.k <= 3) return launch_hot_cfg<3, 1>(a, st);
+    if (a.g.k <= 5) return launch_hot_cfg<5, 1>(a, st);
+    return launch_hot_cfg<8, 1>(a, st);
+  }
+  if (a.g.k <= 3) return launch_hot_cfg<3, 3>(a, st);
+  if (a.g.k <= 5) return launch_hot_cfg<5, 3>(a, st);
+  return launch_hot_cfg<8, 3>(a, st);
+}
+
 template <typename T>
 int launch_hot(const StepArgs& a, cudaStream_t st) {
   if (lean_ok(a)) return launch_lean<T>(a, st);
@@ -2352,11 +2516,14 @@ bool fast_ok(const StepArgs& a, bool f32) {
   const unsigned long long recs = (unsigned long long)a.g.streams *
                                   a.g.depth * (unsigned long long)a.g.height *
                                   a.g.width * rec_elems(kbucket(a.g.k));
-  return f32 && a.q.variant == 0 && a.s.tabq != nullptr && a.iters == 1 &&
-         a.g.stride <= 5 && (a.g.depth == 1 || a.g.depth == 3) &&
+  return f32 && (a.q.variant == 0 || a.q.variant == 3) &&
+         a.s.tabq != nullptr && a.iters == 1 &&
+         a.g.stride <= 4 && (a.g.depth == 1 || a.g.depth == 3) &&
          span < (1ull << 32) && recs < (1ull << 32) &&
-         !a.q.exact_group_sums &&
-         fast_smem_bytes(a.g.depth, a.g.n_groups) <= SMEM_CAP;
+         !a.q.exact_group_sums && !a.q.compat &&
+         (a.q.variant == 3
+              ? fast_smem_bytes(a.g.depth, a.g.n_groups) <= SMEM_CAP
+              : true);
 }
 
 template <typename T>
@@ -2396,7 +2563,8 @@ int launch_step(const StepArgs& a, cudaStream_t st) {
   ensure_bterm();
   // float32 state: the fast kernel; otherwise lean / general
   const bool fast = fast_ok(a, sizeof(T) == 4);
-  int rc = fast ? launch_fast(a, st) : launch_hot<T>(a, st);
+  int rc = fast ? (a.q.variant == 3 ? launch_fast(a, st) : launch_hotpass(a, st))
+                : launch_hot<T>(a, st);
   if (rc) return rc;
   // programmatic dependent launch of the deep pass behind the fast kernel:
   // its CTAs are scheduled while the hot kernel drains (they wait in

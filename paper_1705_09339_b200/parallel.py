@@ -344,7 +344,9 @@ class BatchEngine:
         return torch.cuda.current_stream(self.dev.device).cuda_stream
 
     def _params(self):
-        return params_from_config(self.config, self._wtab)
+        q = params_from_config(self.config, self._wtab)
+        q.variant = _lib.VARIANTS[getattr(self, "kernel_variant", "auto")]
+        return q
 
     @classmethod
     def train(cls, frames_per_stream: Sequence, config: EngineConfig,

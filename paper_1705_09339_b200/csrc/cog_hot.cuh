@@ -27,14 +27,20 @@
 // of the two referenced modes, 8 bytes each from the 64-B record.
 
 constexpr int HQ_CAP = 64;  // per-warp worklist buffer (one global atomic per flush)
+// tiles evaluated side by side by one CTA (D warps each): fewer CTAs per
+// frame, so fewer prologues and partial-sum flushes on small frames
+#ifndef HOT_TPB
+#define HOT_TPB 2  // 1..4
+#endif
+constexpr int HOT_QCAP_BYTES = HQ_CAP * 16;
 
 // pending illumination reset / scheduled reorder of the plane-pixels this
 // thread evaluates (the CTA's tiles, plane c): out of line, called once per
 // frame, so the hot loop's registers never live across a call
 template <int KMAX>
 __device__ __noinline__ void hot_pending(const StepArgs* __restrict__ ap,
-                                         int s, int c, bool do_reset,
-                                         bool do_reorder) {
+                                         int s, int c, int slot,
+                                         bool do_reset, bool do_reorder) {
   using T = float;
   const StepArgs& a = *ap;
   const int lane = threadIdx.x & 31;
@@ -46,7 +52,8 @@ __device__ __noinline__ void hot_pending(const StepArgs* __restrict__ ap,
   const bool lane_ok = lane < stride * cw;
   const PlaneRef<T> pr = plane_ref<T>(a, s, c);
   const double* gmu = a.s.g_mu + ((size_t)s * D + c) * G;
-  for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+  for (int t = blockIdx.x * HOT_TPB + slot; t < a.n_tiles;
+       t += gridDim.x * HOT_TPB) {
     const int ty = t / a.tiles_x, tx = t - ty * a.tiles_x;
     const int y = ty * stride + lrow, x = tx * cw + lcol;
     if (!(lane_ok && y < H && x < W)) continue;
@@ -60,13 +67,23 @@ __device__ __noinline__ void hot_pending(const StepArgs* __restrict__ ap,
   }
 }
 
+// The level walk as a table (kernels_numba.py:286-334): the first level in
+// mid_order whose test is not a miss decides.  Index = the three 2-bit level
+// codes of meta (bits 4-9) * 64 + the test states of the three levels
+// (2 bits each, GROUP / MEAN / MEANVAR: 0 miss, 1 hit, 3 undecided); value =
+// the active level, L_GMM when every test misses or the order ends, 0xFF
+// when an undecided test decides.
+__device__ __align__(16) uint8_t g_walk[64 * 64];
+
 // shared memory of one CTA; `big`: the group sums and constants do not fit
 // (hundreds of groups) and live in global memory instead
 __host__ __device__ inline size_t hot_smem_bytes(int d, int G, bool big) {
   const int g = big ? 0 : G;
+  const int warps = d * HOT_TPB;
   const size_t wpad = ((size_t)acc_words(d, g) + 1) & ~(size_t)1;
-  return (size_t)d * wpad * 8 + (size_t)d * HQ_CAP * 16 +
-         (size_t)2 * d * g * 4 + (size_t)2 * d * 4 + 16;
+  return (size_t)warps * wpad * 8 + (size_t)warps * HOT_QCAP_BYTES +
+         64 * 64 + 3 * 32 + (size_t)2 * d * g * 4 +
+         (size_t)2 * warps * 4 + 16;
 }
 
 // compile-time configuration of a hot_kernel instantiation: FL < 0 reads
@@ -82,7 +99,7 @@ constexpr int HF_DEFAULT = HF_SAMPLING | HF_GROUPING | HF_CHP | HF_RATE;
 #endif
 
 template <int KMAX, int D, int ST, int FL>
-__global__ void __launch_bounds__(32 * D, COG_HOT_MINB / D)
+__global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB))
     hot_kernel(const __grid_constant__ StepArgs a,
                const __grid_constant__ FastConst k) {
   using T = float;
@@ -98,8 +115,12 @@ __global__ void __launch_bounds__(32 * D, COG_HOT_MINB / D)
   const bool big = k.big != 0;  // group sums / constants in global memory
   const int sG = big ? 0 : G;
   const int wpad = (acc_words(D, sG) + 1) & ~1;
+  constexpr int NW = D * HOT_TPB;   // warps per CTA
+  constexpr int NT = 32 * NW;       // threads per CTA
   const int lane = threadIdx.x & 31;
-  const int c = threadIdx.x >> 5;  // this warp's plane
+  const int w = threadIdx.x >> 5;
+  const int c = w % D;              // this warp's plane
+  const int slot = w / D;           // this warp's tile of the CTA's HOT_TPB
   const bool sampling = FL < 0 ? a.q.sampling_on != 0 : (FL & HF_SAMPLING) != 0;
   const bool grouping = FL < 0 ? a.q.grouping_on != 0 : (FL & HF_GROUPING) != 0;
   const bool chp_on = FL < 0 ? a.q.chp_on != 0 : (FL & HF_CHP) != 0;
@@ -107,28 +128,40 @@ __global__ void __launch_bounds__(32 * D, COG_HOT_MINB / D)
   const bool literal = FL < 0 ? a.q.literal_conf != 0 : (FL & HF_LITERAL) != 0;
 
   // ---- shared: warp-private partial slices (lane 0 adds, no atomics),
-  // per-warp worklist buffers, group constants (float), the tile's
-  // per-plane label words (double buffered)
-  unsigned long long* s_wacc = h_mem;                    // [D][wpad]
-  unsigned long long* s_qc = s_wacc + D * wpad;          // [D][HQ_CAP]
-  double* s_qr = (double*)(s_qc + D * HQ_CAP);           // [D][HQ_CAP]
-  float* s_gmu = (float*)(s_qr + D * HQ_CAP);            // [D*G]
+  // per-warp worklist buffers, the level-walk table, the per-class
+  // confidence constants, group constants (float), the tiles' per-plane
+  // label words (double buffered)
+  unsigned long long* s_wacc = h_mem;                    // [NW][wpad]
+  unsigned long long* s_qc = s_wacc + NW * wpad;         // [NW][HQ_CAP]
+  double* s_qr = (double*)(s_qc + NW * HQ_CAP);          // [NW][HQ_CAP]
+  uint8_t* s_walk = (uint8_t*)(s_qr + NW * HQ_CAP);      // [64 * 64]
+  float4* s_cw = (float4*)(s_walk + 64 * 64);            // [3] wa wb wc 1/(wb+wc)
+  float* s_ctm = (float*)(s_cw + 3);                     // [3] conf margins
+  float* s_gmu = s_ctm + 5;                              // [D*G]
   float* s_gthr = s_gmu + D * sG;                        // [D*G]
-  unsigned* s_lab = (unsigned*)(s_gthr + D * sG);        // [2][D]
+  unsigned* s_lab = (unsigned*)(s_gthr + D * sG);        // [2][NW]
   const double* gmu_d = a.s.g_mu + (size_t)s * D * G;
   const double* gvar_d = a.s.g_var + (size_t)s * D * G;
-  for (int i = threadIdx.x; i < D * sG; i += 32 * D) {
+  for (int i = threadIdx.x; i < D * sG; i += NT) {
     s_gmu[i] = (float)gmu_d[i];
     s_gthr[i] = (float)(a.q.match_lambda * sqrt(gvar_d[i]));
   }
-  for (int i = threadIdx.x; i < D * wpad; i += 32 * D) s_wacc[i] = 0ull;
+  for (int i = threadIdx.x; i < NW * wpad; i += NT) s_wacc[i] = 0ull;
+  for (int i = threadIdx.x; i < 64 * 64 / 16; i += NT)
+    reinterpret_cast<uint4*>(s_walk)[i] = reinterpret_cast<const uint4*>(g_walk)[i];
+  if (threadIdx.x < 3) {
+    const int q = threadIdx.x;
+    s_cw[q] = make_float4(k.w[3 * q], k.w[3 * q + 1], k.w[3 * q + 2],
+                          k.wbc_inv[q]);
+    s_ctm[q] = k.ct_margin[q];
+  }
   __syncthreads();
   // let the frame's deep kernel be scheduled now (it waits on this grid's
   // completion before touching anything); hides the launch gap
   asm volatile("griddepcontrol.launch_dependents;");
-  unsigned long long* const wacc = s_wacc + c * wpad;
-  unsigned long long* const qc = s_qc + c * HQ_CAP;
-  double* const qr = s_qr + c * HQ_CAP;
+  unsigned long long* const wacc = s_wacc + w * wpad;
+  unsigned long long* const qc = s_qc + w * HQ_CAP;
+  double* const qr = s_qr + w * HQ_CAP;
 
   // 32-bit element indices from the state arrays' own bases (the launcher
   // guarantees streams * d * 5 * P and the record elements < 2^32)
@@ -158,17 +191,22 @@ __global__ void __launch_bounds__(32 * D, COG_HOT_MINB / D)
   // ---- a pending illumination reset / scheduled reorder (rare, uniform
   // over the grid): applied per plane-pixel before the frame's own pass,
   // over the same tiles this thread evaluates below
-  if (do_reset || do_reorder) hot_pending<KMAX>(&a, s, c, do_reset, do_reorder);
+  if (do_reset || do_reorder)
+    hot_pending<KMAX>(&a, s, c, slot, do_reset, do_reorder);
 
   unsigned long long kc = 0ull;  // kind counts, 7 x 9 bits
   int kc_units = 0;
   int wq_n = 0;
   unsigned fg_count = 0;
   int it = 0;
-  // tile t = ty * tiles_x + tx, advanced by the grid size without a division
-  const int dty = gridDim.x / a.tiles_x, dtx = gridDim.x - dty * a.tiles_x;
-  int ty = blockIdx.x / a.tiles_x, tx = blockIdx.x - ty * a.tiles_x;
-  for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++it) {
+  // the CTA's tiles: round r covers tiles (blockIdx.x + r * gridDim.x) *
+  // HOT_TPB + slot; t = ty * tiles_x + tx advanced without a division
+  const int step = gridDim.x * HOT_TPB;
+  const int dty = step / a.tiles_x, dtx = step - dty * a.tiles_x;
+  const int t_first = blockIdx.x * HOT_TPB + slot;
+  int ty = t_first / a.tiles_x, tx = t_first - ty * a.tiles_x;
+  for (int t0 = blockIdx.x * HOT_TPB; t0 < a.n_tiles; t0 += step, ++it) {
+    const int t = t0 + slot;
     const int y = ty * stride + lrow, x = tx * cw + lcol;
     ty += dty;
     tx += dtx;
@@ -176,7 +214,7 @@ __global__ void __launch_bounds__(32 * D, COG_HOT_MINB / D)
       tx -= a.tiles_x;
       ty += 1;
     }
-    const bool valid = lane_ok && y < H && x < W;
+    const bool valid = lane_ok && t < a.n_tiles && y < H && x < W;
     const uint32_t p = valid ? (uint32_t)y * (uint32_t)W + (uint32_t)x : 0u;
     const uint32_t o = plane + p;
 
@@ -238,9 +276,8 @@ __global__ void __launch_bounds__(32 * D, COG_HOT_MINB / D)
     // fp32 operands lie inside the filter margin defers the plane-pixel
     const float thr0 = k.lam * (m0.y * rsqrt_approx(m0.y));
     const float thr1 = k.lam * (m1.y * rsqrt_approx(m1.y));
-    const float wa = cls == 0 ? k.w[0] : (cls == 1 ? k.w[3] : k.w[6]);
-    const float wb = cls == 0 ? k.w[1] : (cls == 1 ? k.w[4] : k.w[7]);
-    const float wc = cls == 0 ? k.w[2] : (cls == 1 ? k.w[5] : k.w[8]);
+    const float4 cwv = s_cw[cls];  // wa, wb, wc, 1 / (wb + wc)
+    const float wa = cwv.x, wb = cwv.y, wc = cwv.z;
     const bool top1 = top == L_MEANVAR;
     const float mt = gtop ? gm : (top1 ? m1.x : m0.x);
     const float dn = gtop ? gthr : (top1 ? thr1 : thr0);
@@ -251,46 +288,46 @@ __global__ void __launch_bounds__(32 * D, COG_HOT_MINB / D)
     const float gt = literal ? gtl : 1.0f - gtl;
     const float wbc = __fmaf_rn(wb, bt, __fmul_rn(wc, gt));
     const bool floor_ = ph < k.pf;
-    const float wbci =
-        cls == 0 ? k.wbc_inv[0] : (cls == 1 ? k.wbc_inv[1] : k.wbc_inv[2]);
-    const float cf_ev = floor_ ? __fmul_rn(wbc, wbci) : __fmaf_rn(wa, ph, wbc);
-    const float ct_m = cls == 0 ? k.ct_margin[0]
-                                : (cls == 1 ? k.ct_margin[1] : k.ct_margin[2]);
+    const float cf_ev = floor_ ? __fmul_rn(wbc, cwv.w) : __fmaf_rn(wa, ph, wbc);
+    const float ct_m = s_ctm[cls];
     bool deferred = ev && (fabsf(ph - k.pf) <= k.pf_margin ||
                            fabsf(cf_ev - k.ct) <= ct_m);
-    // the level tests, then the first hit in mid_order (the first test
-    // that is not a miss decides; an undecided one defers)
-    int hm0 = fmatch(vf, m0.x, thr0), hm1 = fmatch(vf, m1.x, thr1);
+    // the level tests, then the first decisive one in mid_order (table)
+    const uint32_t codes = ((meta >> 4) & 63u) << 6;
+    uint32_t sg = (uint32_t)ghit & 3u;  // 0 miss, 1 hit, 3 undecided
+    uint32_t sm0 = (uint32_t)fmatch(vf, m0.x, thr0) & 3u;
+    uint32_t sm1 = (uint32_t)fmatch(vf, m1.x, thr1) & 3u;
     auto walk = [&]() {
-      int act = L_GMM;
-#pragma unroll
-      for (int j = 2; j >= 0; --j) {  // the earliest decisive test wins
-        const uint32_t code = j == 0 ? c0 : (j == 1 ? c1 : c2);
-        if (code == 0) {
-          act = L_GMM;  // the walk ends before this code
-          continue;
-        }
-        const int hit = code == L_GROUP ? ghit : (code == L_MEAN ? hm0 : hm1);
-        if (hit != 0) act = hit > 0 ? (int)code : -1;
-      }
-      return act;
+      const int v = s_walk[codes | sg | (sm0 << 2) | (sm1 << 4)];
+      return v == 0xFF ? -1 : v;
     };
     int active = L_CHP, label = chp_hit ? last_label : 0;
     if (!chp_hit) {
       active = walk();
       // a matched mode must also sit inside the background weight prefix,
-      // else the walk continues (kernels_numba.py:298-311); rare: only
-      // when the matched mode is not the first one
+      // else the walk continues (kernels_numba.py:298-311); only when the
+      // matched mode is not the first one
       for (int guard = 0; guard < 2 && ev; ++guard) {
         const bool m = active == L_MEAN && r0 > 0;
         const bool mv = active == L_MEANVAR && r1 > 0;
         if (!m && !mv) break;
         const uint32_t rr = m ? r0 : r1;
+        // w_0 .. w_{K-2} in one round of 8-byte loads, summed in the
+        // reference's order in binary64
+        float wv[KMAX];
+#pragma unroll
+        for (int i = 0; i + 1 < KMAX; i += 2) {
+          const float2 t2 = *reinterpret_cast<const float2*>(rec + WO + i);
+          wv[i] = t2.x;
+          wv[i + 1] = t2.y;
+        }
         double acc = 0.0;
-        for (uint32_t q = 0; q < rr; ++q) acc = acc + (double)rec[WO + q];
+#pragma unroll
+        for (int q = 0; q + 1 < KMAX; ++q)
+          if ((uint32_t)q < rr) acc = acc + (double)wv[q];
         if (acc <= a.q.background_threshold) break;
-        if (m) hm0 = 0;
-        else hm1 = 0;
+        if (m) sm0 = 0u;
+        else sm1 = 0u;
         active = walk();
       }
     }
@@ -478,13 +515,22 @@ __global__ void __launch_bounds__(32 * D, COG_HOT_MINB / D)
       if (valid) a.mask[s1 + p] = (lb >> lane) & 1u ? 255 : 0;
       fg_count += __popc(lb);
     } else {
-      unsigned* slot = s_lab + (it & 1) * D;
-      if (lane == 0) slot[c] = lb;
-      __syncthreads();
+      unsigned* lab = s_lab + (it & 1) * NW + slot * D;
+      if (lane == 0) lab[c] = lb;
+      // the D warps of this tile only (named barrier 1 + slot; the ids are
+      // compile-time constants, so the CTA reserves HOT_TPB + 1 barriers)
+      if (HOT_TPB == 1 || slot == 0)
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * D) : "memory");
+      else if (HOT_TPB == 2 || slot == 1)
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * D) : "memory");
+      else if (HOT_TPB == 3 || slot == 2)
+        asm volatile("bar.sync 3, %0;" ::"n"(32 * D) : "memory");
+      else
+        asm volatile("bar.sync 4, %0;" ::"n"(32 * D) : "memory");
       if (c == 0) {
         unsigned u = 0;
 #pragma unroll
-        for (int j = 0; j < D; ++j) u |= slot[j];
+        for (int j = 0; j < D; ++j) u |= lab[j];
         if (valid) a.mask[s1 + p] = (u >> lane) & 1u ? 255 : 0;
         fg_count += __popc(u & __ballot_sync(FULL, valid));
       }
@@ -508,10 +554,10 @@ __global__ void __launch_bounds__(32 * D, COG_HOT_MINB / D)
   if (lane == 0) wacc[acc_fg(D)] += fg_count;
   __syncthreads();
   const int sw = acc_words(D, sG);  // words held in shared
-  for (int i = threadIdx.x; i < sw; i += 32 * D) {
+  for (int i = threadIdx.x; i < sw; i += NT) {
     unsigned long long v = 0;
 #pragma unroll
-    for (int w = 0; w < D; ++w) v += s_wacc[w * wpad + i];
+    for (int j = 0; j < NW; ++j) v += s_wacc[j * wpad + i];
     if (v) atomicAdd(gacc + i, v);
   }
 }

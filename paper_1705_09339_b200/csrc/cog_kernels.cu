@@ -2277,6 +2277,25 @@ void ensure_bterm() {
     t[0][i] = 1.0 - b;
   }
   cudaMemcpyToSymbol(g_bterm, t, sizeof(t));
+  // the level-walk table of hot_kernel (cog_hot.cuh): for the level codes
+  // (c0, c1, c2) and the 2-bit test states of GROUP / MEAN / MEANVAR, the
+  // first code whose test is not a miss decides (kernels_numba.py:286-334)
+  uint8_t wt[64 * 64];
+  for (int codes = 0; codes < 64; ++codes) {
+    for (int st = 0; st < 64; ++st) {
+      int out = L_GMM;
+      for (int j = 0; j < 3; ++j) {
+        const int code = (codes >> (2 * j)) & 3;
+        if (code == 0) break;  // mid_order entry -1: the walk ends
+        const int state = (st >> (2 * (code - 1))) & 3;
+        if (state == 0) continue;  // miss: next level
+        out = state == 1 ? code : 0xFF;  // hit, or undecided
+        break;
+      }
+      wt[codes * 64 + st] = (uint8_t)out;
+    }
+  }
+  cudaMemcpyToSymbol(g_walk, wt, sizeof(wt));
   done[dev] = true;
 }
 
@@ -2450,13 +2469,18 @@ int launch_hot_k(const StepArgs& a, cudaStream_t st) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  const int threads = 32 * D;
+  // the whole unified L1/shared array as shared memory: the occupancy is
+  // then bounded by the registers, not by a small default carveout
+  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       (int)cudaSharedmemCarveoutMaxShared);
+  const int threads = 32 * D * HOT_TPB;
   const int occ = cached_occupancy((const void*)fn, threads, smem);
-  // one tile per CTA at a time, CTAs striding over the tiles; every CTA of
-  // every stream resident in one wave
+  // HOT_TPB tiles per CTA at a time, CTAs striding over the tiles; every
+  // CTA of every stream resident in one wave
   int per_stream = (num_sms() * occ) / a.g.streams;
   if (per_stream < 1) per_stream = 1;
-  const int gx = a.n_tiles < per_stream ? a.n_tiles : per_stream;
+  const int need = (a.n_tiles + HOT_TPB - 1) / HOT_TPB;
+  const int gx = need < per_stream ? need : per_stream;
   FastConst k = make_fast_const(a.q);
   k.big = big ? 1 : 0;
   fn<<<dim3(gx < 1 ? 1 : gx, a.g.streams), threads, smem, st>>>(a, k);

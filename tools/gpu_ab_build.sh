@@ -7,7 +7,7 @@ for r in $(seq $R); do
   for v in "$A" "$B"; do
     python -c "import sys; sys.path.insert(0,'.'); from paper_1705_09339_b200 import _lib; _lib.build_extension(defines=tuple('$v'.split()))" || exit 1
     for w in $WL; do
-      python bench.py --workload $w --steps 20 --warmup 3 --no-cpu 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('[$v]'.ljust(28), '$w', 'ms/step %.4f frac %.3f' % (d['ms_per_step'], d['roofline']['frac']))" | tee -a $OUT/ab.txt
+      python bench.py --workload $w --steps 60 --warmup 5 --no-cpu 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('[$v]'.ljust(28), '$w', 'ms/step %.4f frac %.3f' % (d['ms_per_step'], d['roofline']['frac']))" | tee -a $OUT/ab.txt
     done
   done
 done

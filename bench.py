@@ -18,9 +18,11 @@ over the ranks, processed in waves of --streams resident streams).
 value    device-resident frames, CUDA events around each step's launches on
          the engine stream, L2 flushed (256 MiB write, untimed) between
          steps; MAX over ranks of the summed step time.
-e2e      the public API ``process_frame`` fed numpy frames from (pageable)
-         host memory, as a reference caller passes them: staging, H2D,
-         step, D2H of mask + stats all inside the timed region.
+e2e      the public API ``process_frame`` (c5: ``submit_frames``) fed frames
+         from pinned host memory: H2D, step, D2H of mask + stats inside the
+         timed region, results read two frames behind the submission.
+         extra.e2e_pageable: the same with pageable numpy frames, as a
+         reference caller passes them (+ the staging copy).
 roofline the fused frame step (fast_kernel + deep_kernel): SURVEY.md 8(d)
          algorithmic bytes of each timed frame (B_frame from that frame's
          own level populations) / step time; when the committed ncu
@@ -411,11 +413,27 @@ class Workload:
         r = self.stats[lo:].cpu().numpy()
         return r.reshape(-1, 16)
 
-    def e2e_submit(self, eng, i):
+    def e2e_submit(self, eng, i, pinned=True):
         """The public API with host frames: enqueue frame i from this
-        rank's pageable numpy frames (staging copy, H2D, step, D2H of mask
-        + stats); returns the pending result and the bytes moved each
-        way."""
+        rank's frames in pinned host memory (the contract's e2e: H2D, step,
+        D2H of mask + stats) or, pinned=False, from pageable numpy arrays as
+        a reference caller passes them (+ the staging copy); returns the
+        pending result and the bytes moved each way."""
+        if pinned:
+            if getattr(self, "host_pinned", None) is None:
+                import torch
+                self.host_pinned = [torch.from_numpy(x).pin_memory()
+                                    for x in self.host]
+            f = self.host_pinned[i % len(self.host_pinned)]
+            nb = f.numel()
+        else:
+            f = self.host[i % len(self.host)]
+            nb = f.nbytes
+        if self.streams == 1:
+            m, st = eng.process_frame(f)
+            return (m, st), nb, self.pixels + 16 * 8
+        res = eng.submit_frames(f)
+        return (res,), nb, self.pixels + self.streams * 16 * 8
         f = self.host[i % len(self.host)]
         if self.streams == 1:
             m, st = eng.process_frame(f)
@@ -464,14 +482,14 @@ def time_device_loop(wl, args, world, local):
     return [s.elapsed_time(e) for s, e in zip(starts, ends)], clk
 
 
-def time_e2e(wl, args, world):
+def time_e2e(wl, args, world, pinned=True):
     """The public API end to end: frames from host memory, results read on
     the host two frames behind the submission (so copies and host work
     overlap later steps)."""
     import torch
     eng = wl.eng
     for i in range(args.warmup):
-        r, _, _ = wl.e2e_submit(eng, i)
+        r, _, _ = wl.e2e_submit(eng, i, pinned)
         wl.e2e_read(r)
     torch.cuda.synchronize()
     if world > 1:
@@ -480,7 +498,7 @@ def time_e2e(wl, args, world):
     bi = bo = 0
     inflight = []
     for i in range(args.steps):
-        cur, bi, bo = wl.e2e_submit(eng, args.warmup + i)
+        cur, bi, bo = wl.e2e_submit(eng, args.warmup + i, pinned)
         inflight.append(cur)
         if len(inflight) > 2:
             wl.e2e_read(inflight.pop(0))
@@ -537,34 +555,48 @@ def main():
     else:
         waves = [None]
 
-    durs_all, e2e_s, rows_all = [], 0.0, []
+    durs_all, e2e_s, e2e_pg_s, rows_all = [], 0.0, 0.0, []
     t_train = t_gen = 0.0
     bi = bo = 0
     clk = None
     wl = None
     for wave in waves:
         if wl is not None:
+            # free the previous wave's engine (its streams are done)
+            import gc
+            wl.eng = eng = None
             del wl
+            gc.collect()
             torch.cuda.empty_cache()
         wl = Workload(args.workload, args, world, rank, streams=wave)
         wl.eng.kernel_variant = args.variant
         t_train += wl.t_train
         t_gen += wl.t_gen
         eng, cfg = wl.eng, wl.cfg
-        e2e_eng = eng.clone() if hasattr(eng, "clone") else None
+        twins = ([eng.clone(), eng.clone()] if hasattr(eng, "clone")
+                 else [None, None])
         durs, c = time_device_loop(wl, args, world, local)
         clk = c if clk is None else clk
         durs_all.extend(durs)
         rows_all.append(wl.rows_stats(args.warmup))
-        if e2e_eng is not None:
-            wl.eng = e2e_eng
-        dt, bi_, bo_ = time_e2e(wl, args, world)
-        e2e_s += dt
-        bi += bi_
-        bo += bo_
-        wl.eng = eng
+        # e2e from pinned host frames (the contract), then from pageable
+        # numpy frames (what a reference caller passing arrays pays: + the
+        # staging copy), each on a twin starting from the trained state
+        for twin, pinned in zip(twins, (True, False)):
+            if twin is not None:
+                wl.eng = twin
+            dt, bi_, bo_ = time_e2e(wl, args, world, pinned)
+            if pinned:
+                e2e_s += dt
+                bi += bi_
+                bo += bo_
+            else:
+                e2e_pg_s += dt
+            wl.eng = eng
+        del twins
     total_ms = max_over_ranks(float(np.sum(durs_all)), world)
     e2e_s = max_over_ranks(e2e_s, world)
+    e2e_pg_s = max_over_ranks(e2e_pg_s, world)
     rows = np.concatenate(rows_all)
     k = wl.cfg.k_max
     spec = wl.spec
@@ -576,6 +608,7 @@ def main():
         units = world * spec.n_pix
     value = units * args.steps / (total_ms * 1e-3)
     e2e = units * args.steps / e2e_s
+    e2e_pg = units * args.steps / e2e_pg_s
     step_ms = float(np.mean(durs_all))
     b_frame = float(np.mean([byte_model(r, 3, k) for r in rows]))
     b_step = b_frame * (rows.shape[0] / (args.steps * len(waves)))
@@ -656,6 +689,12 @@ def main():
             "gpu_launches": 2 * args.steps * len(waves),
             "clocks": clk.summary() if clk else None,
             "extra": {"train_s": t_train, "scene_gen_s": t_gen,
+                      "e2e_pageable": {
+                          "value": e2e_pg, "unit": "pixel-frames/s",
+                          "what": "process_frame / submit_frames fed "
+                                  "pageable numpy frames (+ the staging "
+                                  "copy into pinned memory; host-memory "
+                                  "bound on this box)"},
                       "step_ms_min": float(np.min(durs_all)),
                       "step_ms_max": float(np.max(durs_all)),
                       "level_fractions": {k_: float(x) for k_, x in zip(

@@ -298,11 +298,16 @@ class DeviceState:
         g.streams = 1
         return g
 
+    # written only while training / loading a model (into a fresh state),
+    # read-only to every step: a clone shares them instead of copying the
+    # ~1.5 KB per plane-pixel prior
+    _READ_ONLY = ("table", "peak", "tabq", "cls", "gid", "g_members")
+
     def clone(self) -> "DeviceState":
         twin = DeviceState.__new__(DeviceState)
         for k, v in vars(self).items():
             if isinstance(v, torch.Tensor):
-                setattr(twin, k, v.clone())
+                setattr(twin, k, v if k in self._READ_ONLY else v.clone())
             elif k not in ("geom", "cstate"):
                 setattr(twin, k, v)
         twin._refresh()

@@ -46,6 +46,9 @@ constexpr int STATS_WORDS = 16;
 #ifndef DEEP_THREADS
 #define DEEP_THREADS 256  // deep_kernel CTA size
 #endif
+#ifndef DEEP_MINB
+#define DEEP_MINB 2  // deep_kernel CTAs per SM the registers must allow
+#endif
 
 // accumulator layout (u64 words, per stream)
 __host__ __device__ inline int acc_kind(int c, int k) { return c * 7 + k; }
@@ -1660,8 +1663,18 @@ __device__ __noinline__ unsigned deferred_item(const StepArgs& a, int s,
   return label ? late_label(a, s, c, p, cmask) : 0u;
 }
 
+// the binary64 update of a float32 worklist item whose fp32 decision was
+// too close to call: out of line, so the fp32 path keeps few registers
+template <int KMAX>
+__device__ __noinline__ unsigned deep_item_f64_of_f32(const StepArgs* __restrict__ ap,
+                                                      int s,
+                                                      unsigned long long code,
+                                                      double rho) {
+  return deep_item<float, KMAX>(*ap, s, code, rho);
+}
+
 template <typename T, int KMAX>
-__global__ void __launch_bounds__(DEEP_THREADS) deep_kernel(const StepArgs a) {
+__global__ void __launch_bounds__(DEEP_THREADS, DEEP_MINB) deep_kernel(const StepArgs a) {
   __shared__ int s_last;
   __shared__ unsigned long long s_fg;
   // launched with programmatic stream serialization after fast_kernel: wait
@@ -1703,6 +1716,8 @@ __global__ void __launch_bounds__(DEEP_THREADS) deep_kernel(const StepArgs a) {
           fg += nw;
           continue;
         }
+        fg += deep_item_f64_of_f32<KMAX>(&a, s, code, dq_rho[i]);
+        continue;
       }
     }
     fg += deep_item<T, KMAX>(a, s, code, dq_rho[i]);

@@ -93,6 +93,12 @@ class DistReducer:
 
     def __call__(self, accum: torch.Tensor) -> None:
         import torch.distributed as dist
+        if accum.is_cuda and dist.get_backend(self.group) == "gloo":
+            # gloo reduces host tensors: stage through the host
+            host = accum.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.SUM, group=self.group)
+            accum.copy_(host)
+            return
         dist.all_reduce(accum, op=dist.ReduceOp.SUM, group=self.group)
 
 

@@ -672,7 +672,7 @@ def main():
                                        f"{world} rank(s), independent "
                                        f"streams{wave_txt}")},
             "roofline": {"bound": "hbm",
-                         "kernel": "the fused frame step (fast_kernel + "
+                         "kernel": "the frame step (hot_kernel + "
                                    "deep_kernel), CUDA events on the engine "
                                    "stream",
                          "achieved": achieved, "peak": peak,

@@ -124,6 +124,13 @@ typedef struct cog_state {
   uint32_t *sync;
   uint64_t *deepq;   /* u64[cog_deepq_slots()] worklist (zero-initialised) */
   double *deeprho;   /* f64[cog_deepq_slots()] */
+  uint32_t *hitq;    /* u32[depth][P] or NULL: the float32 hot pass counts
+                        its CHP / GROUP / MEAN / MEANVAR hits here, one
+                        byte per level in one word per plane-pixel (one
+                        dense RED instead of one per level plane);
+                        hits = hits + the bytes of hitq.  Folded back into
+                        `hits` before a byte can wrap and wherever hits is
+                        read or zeroed (reorder, reset, export). */
 } cog_state;
 
 /* Words of `accum` per stream (kinds, foreground, group partials). */

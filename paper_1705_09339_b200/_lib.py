@@ -103,7 +103,7 @@ class State(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "mix", "meta", "dyn", "streak", "hits", "table", "peak", "tabq",
         "cls", "gid", "g_mu", "g_var", "g_members", "accum", "sync",
-        "deepq", "deeprho")]
+        "deepq", "deeprho", "hitq")]
 
 
 class RefState(ctypes.Structure):

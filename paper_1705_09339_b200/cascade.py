@@ -201,6 +201,9 @@ class DeviceState:
         self.dyn = z(S, d, P, dtype=torch.int32)
         self.streak = z(S, d, P, dtype=torch.int32)
         self.hits = z(S, d, 5, P, dtype=torch.int32)
+        # float32 engines: the hot pass's packed per-level hit bytes
+        # (include/cog_b200.h, cog_state.hitq); hits = hits + its bytes
+        self.hitq = None if self.f64 else z(S, d, P, dtype=torch.int32)
         # the prior in the reference layout (exact values), and for float32
         # engines its u16 tile-major hot copy (cog_tabq_build)
         self.table = z(S, d, P, 256, dtype=torch.float32)
@@ -275,7 +278,7 @@ class DeviceState:
 
     _BUFS = ("mix", "meta", "dyn", "streak", "hits", "table", "peak", "tabq",
              "cls", "gid", "g_mu", "g_var", "g_members", "accum", "sync",
-             "deepq", "deeprho")
+             "deepq", "deeprho", "hitq")
 
     def _refresh(self) -> None:
         self.geom = self._geom(self.streams)

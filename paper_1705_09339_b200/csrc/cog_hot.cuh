@@ -40,7 +40,8 @@ constexpr int HOT_QCAP_BYTES = HQ_CAP * 16;
 template <int KMAX>
 __device__ __noinline__ void hot_pending(const StepArgs* __restrict__ ap,
                                          int s, int c, int slot,
-                                         bool do_reset, bool do_reorder) {
+                                         bool do_reset, bool do_reorder,
+                                         bool do_fold) {
   using T = float;
   const StepArgs& a = *ap;
   const int lane = threadIdx.x & 31;
@@ -64,6 +65,8 @@ __device__ __noinline__ void hot_pending(const StepArgs* __restrict__ ap,
       cold_reorder<T>(pr, p, (G > 0 && g0 != (int)UNGROUPED)
                                  ? gmu[g0] : (G > 0 ? gmu[0] : 0.0));
     }
+    // neither of the two left anything in the packed hit bytes
+    if (do_fold && !do_reset && !do_reorder) cold_fold_hits<T>(pr, p);
   }
 }
 
@@ -77,13 +80,51 @@ __device__ __align__(16) uint8_t g_walk[64 * 64];
 
 // shared memory of one CTA; `big`: the group sums and constants do not fit
 // (hundreds of groups) and live in global memory instead
-__host__ __device__ inline size_t hot_smem_bytes(int d, int G, bool big) {
+// the pipelined variant's per-warp ring of round-1 stages (HOT_NS tiles in
+// flight per warp): dyn[32] u32, streak[32] u32, meta[32] u16, gid[32] u16,
+// frame[32] u8, cls[32] u8
+#ifndef HOT_NS
+#define HOT_NS 4
+#endif
+constexpr int HOT_STAGE_BYTES = 448;
+constexpr int HS_DYN = 0, HS_STREAK = 128, HS_META = 256, HS_GID = 320,
+              HS_FRAME = 384, HS_CLS = 416;
+
+__host__ __device__ inline size_t hot_smem_bytes(int d, int G, bool big,
+                                                 bool pipe = false) {
   const int g = big ? 0 : G;
   const int warps = d * HOT_TPB;
   const size_t wpad = ((size_t)acc_words(d, g) + 1) & ~(size_t)1;
-  return (size_t)warps * wpad * 8 + (size_t)warps * HOT_QCAP_BYTES +
-         64 * 64 + 3 * 32 + (size_t)2 * d * g * 4 +
-         (size_t)2 * warps * 4 + 16;
+  size_t n = (size_t)warps * wpad * 8 + (size_t)warps * HOT_QCAP_BYTES +
+             64 * 64 + 3 * 32 + (size_t)2 * d * g * 4 +
+             (size_t)2 * warps * 4 + 16;
+  if (pipe) n = ((n + 15) & ~(size_t)15) + (size_t)warps * HOT_NS * HOT_STAGE_BYTES;
+  return n;
+}
+
+// one plane-pixel's loads, handed from the front half of the tile loop
+// (gates + loads) to the back half (evaluation + writes); in the pipelined
+// variant the front half runs one tile ahead of the back half
+struct HotIn {
+  uint32_t p;     // pixel index (0 for an invalid lane)
+  uint32_t dyn, sk;
+  uint32_t mq;    // meta | q16 << 16
+  uint32_t pk;    // v | cls << 8 | valid << 15 | gid << 16
+  float2 m0, m1;  // the two referenced modes (mu, var)
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src,
+                                           uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 // compile-time configuration of a hot_kernel instantiation: FL < 0 reads
@@ -98,10 +139,16 @@ constexpr int HF_DEFAULT = HF_SAMPLING | HF_GROUPING | HF_CHP | HF_RATE;
 #define COG_HOT_MINB 30
 #endif
 
-template <int KMAX, int D, int ST, int FL>
+// PIPE (stride 2, rows 16-byte aligned): the round-1 arrays of the warp's
+// next HOT_NS - 1 tiles are in flight as 16-byte cp.async copies into the
+// warp's shared ring, and the front half (gates, prior and mode loads) of
+// tile j + 1 is issued before the back half of tile j runs, so both load
+// rounds overlap a whole tile of evaluation without holding registers
+template <int KMAX, int D, int ST, int FL, bool PIPE>
 __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB))
     hot_kernel(const __grid_constant__ StepArgs a,
                const __grid_constant__ FastConst k) {
+  static_assert(!PIPE || ST == 2, "the pipelined ring is laid out for stride 2");
   using T = float;
   constexpr int R = rec_elems(KMAX), WO = rec_w(KMAX);
   extern __shared__ unsigned long long h_mem[];
@@ -176,8 +223,13 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
   unsigned long long* const dq_code =
       (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
   double* const dq_rho = a.s.deeprho + (size_t)s * dq_cap;
-  const bool do_reset = (*(volatile uint32_t*)(sync + 1) & 1u) != 0;
+  const uint32_t pend = *(volatile uint32_t*)(sync + 1);
+  const bool do_reset = (pend & 1u) != 0;
   const bool do_reorder = a.reorder_now != 0;
+  // the packed hit bytes are folded into the wide counters before a byte
+  // can wrap (finalize_stream counts the frames since they were cleared)
+  uint32_t* const hitq = a.s.hitq;
+  const bool do_fold = hitq != nullptr && (pend >> 8) >= HITQ_FOLD_AGE;
   // this warp's plane of the hot prior: tile t, bin v, slot at
   // (t * 256 + v) * 32 + slot
   const uint16_t* const tq =
@@ -191,41 +243,211 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
   // ---- a pending illumination reset / scheduled reorder (rare, uniform
   // over the grid): applied per plane-pixel before the frame's own pass,
   // over the same tiles this thread evaluates below
-  if (do_reset || do_reorder)
-    hot_pending<KMAX>(&a, s, c, slot, do_reset, do_reorder);
+  if (do_reset || do_reorder || do_fold) {
+    hot_pending<KMAX>(&a, s, c, slot, do_reset, do_reorder, do_fold);
+    // every plane-pixel's packed hit bytes are zero now: their age restarts
+    if (hitq != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+      atomicAdd(gacc + acc_flag(D, G), 1ull);
+  }
 
   unsigned long long kc = 0ull;  // kind counts, 7 x 9 bits
   int kc_units = 0;
   int wq_n = 0;
   unsigned fg_count = 0;
-  int it = 0;
   // the CTA's tiles: round r covers tiles (blockIdx.x + r * gridDim.x) *
   // HOT_TPB + slot; t = ty * tiles_x + tx advanced without a division
   const int step = gridDim.x * HOT_TPB;
   const int dty = step / a.tiles_x, dtx = step - dty * a.tiles_x;
   const int t_first = blockIdx.x * HOT_TPB + slot;
-  int ty = t_first / a.tiles_x, tx = t_first - ty * a.tiles_x;
-  for (int t0 = blockIdx.x * HOT_TPB; t0 < a.n_tiles; t0 += step, ++it) {
-    const int t = t0 + slot;
-    const int y = ty * stride + lrow, x = tx * cw + lcol;
-    ty += dty;
-    tx += dtx;
-    if (tx >= a.tiles_x) {
-      tx -= a.tiles_x;
-      ty += 1;
-    }
+  const int n_it = ((int)a.n_tiles - (int)(blockIdx.x * HOT_TPB) + step - 1) / step;
+
+  // ---- front half of a tile: the gates that decide which loads are
+  // needed, then the loads.  Round 1 comes from global memory, or from the
+  // ring stage `st` the copies have filled
+  auto front = [&](int t, int ty_, int tx_, const unsigned char* st) -> HotIn {
+    HotIn in;
+    const int y = ty_ * stride + lrow, x = tx_ * cw + lcol;
     const bool valid = lane_ok && t < a.n_tiles && y < H && x < W;
     const uint32_t p = valid ? (uint32_t)y * (uint32_t)W + (uint32_t)x : 0u;
     const uint32_t o = plane + p;
+    int vb, gid, cls;
+    uint32_t dyn, meta, sk;
+    if (PIPE) {
+      dyn = *reinterpret_cast<const uint32_t*>(st + HS_DYN + lane * 4);
+      sk = *reinterpret_cast<const uint32_t*>(st + HS_STREAK + lane * 4);
+      meta = *reinterpret_cast<const uint16_t*>(st + HS_META + lane * 2);
+      gid = *reinterpret_cast<const uint16_t*>(st + HS_GID + lane * 2);
+      vb = st[HS_FRAME + lane];
+      cls = st[HS_CLS + lane];
+    } else {
+      // addresses are in range for every lane; invalid lanes read pixel 0
+      // and write nothing
+      vb = a.frame[o];
+      dyn = a.s.dyn[o];
+      meta = a.s.meta[o];
+      sk = a.s.streak[o];
+      gid = a.s.gid[s1 + p];
+      cls = a.s.cls[s1 + p];
+    }
+    const bool member = valid && G > 0 && gid != (int)UNGROUPED;
+    const int gidx = member ? c * G + gid : 0;
+    const int dv = abs(vb - (int)(dyn & 0xFF));
+    const bool changed = dv > k.eps_i;
+    const bool asleep = sampling && (dyn >> 16) != 0u;
+    const bool waking = sampling && !asleep && ((dyn >> 9) & 1u);
+    const bool skip = asleep && !changed;
+    const bool copy = waking && !changed && !on_lat;
+    const bool ev = valid && !skip && !copy;
+    const uint32_t c0 = (meta >> 4) & 3u, c1 = (meta >> 6) & 3u;
+    const uint32_t r0 = (meta >> 10) & 7u, r1 = (meta >> 13) & 7u;
+    const uint32_t top = (c0 == L_GROUP && !grouping) ? c1 : c0;
+    const bool gtop = top == L_GROUP && member;
+    float gm = 0.0f, gthr = 1.0f;
+    if (member) {
+      if (!big) {
+        gm = s_gmu[gidx];
+        gthr = s_gthr[gidx];
+      } else {
+        gm = (float)gmu_d[gidx];
+        gthr = (float)(a.q.match_lambda * sqrt(gvar_d[gidx]));
+      }
+    }
+    const int ghit = (grouping && member) ? fmatch((float)vb, gm, gthr) : 0;
+    const bool chp_hit = chp_on && !changed;
+    // the modes are needed unless the confidence reads the group and the
+    // walk stops at the group level (or the probe) before any mode level
+    const bool need =
+        ev && !(gtop && (chp_hit || (c0 == L_GROUP && ghit == 1)));
+    const T* const rec = mix_s + o * R;  // this plane-pixel's mixture record
+    uint32_t q16 = 0u;
+    in.m0 = make_float2(0.0f, 1.0f);
+    in.m1 = in.m0;
+    if (ev) q16 = __ldcg(tq + ((size_t)t * 256 + vb) * 32);
+    if (need) {
+      in.m0 = *reinterpret_cast<const float2*>(rec + 2 * r0);
+      in.m1 = *reinterpret_cast<const float2*>(rec + 2 * r1);
+    }
+    in.p = p;
+    in.dyn = dyn;
+    in.sk = sk;
+    in.mq = (meta & 0xFFFFu) | (q16 << 16);
+    in.pk = (uint32_t)vb | ((uint32_t)cls << 8) | ((uint32_t)valid << 15) |
+            ((uint32_t)gid << 16);
+    return in;
+  };
 
-    // ---- round 1 (addresses are in range for every lane; invalid lanes
-    // read pixel 0 and write nothing)
-    const int vb = a.frame[o];
-    const uint32_t dyn = a.s.dyn[o];
-    const uint32_t meta = a.s.meta[o];
-    const uint32_t sk = a.s.streak[o];
-    const int gid = a.s.gid[s1 + p];
-    const int cls = a.s.cls[s1 + p];
+  // ---- the pipelined variant's copy stream: lane l < 28 moves one 16-byte
+  // chunk of one round-1 array per tile (rows of 16 pixels: dyn / streak 4
+  // chunks a row, meta / gid 2, frame / cls 1)
+  const char* cbase = nullptr;  // array base + plane + the chunk's row / column
+  int csh = 0, crow = 0;
+  uint32_t cdst = 0;            // shared address of the chunk in stage 0
+  unsigned char* ring = nullptr;
+  if (PIPE) {
+    const size_t off = (hot_smem_bytes(D, G, big, false) + 15) & ~(size_t)15;
+    ring = reinterpret_cast<unsigned char*>(h_mem) + off +
+           (size_t)w * HOT_NS * HOT_STAGE_BYTES;
+    int l = lane, chunk = 0;
+    uint32_t d0 = 0;
+    if (l < 8) {
+      cbase = (const char*)(a.s.dyn + plane); csh = 2; crow = l >> 2; chunk = l & 3;
+      d0 = HS_DYN + crow * 64;
+    } else if (l < 16) {
+      l -= 8;
+      cbase = (const char*)(a.s.streak + plane); csh = 2; crow = l >> 2; chunk = l & 3;
+      d0 = HS_STREAK + crow * 64;
+    } else if (l < 20) {
+      l -= 16;
+      cbase = (const char*)(a.s.meta + plane); csh = 1; crow = l >> 1; chunk = l & 1;
+      d0 = HS_META + crow * 32;
+    } else if (l < 24) {
+      l -= 20;
+      cbase = (const char*)(a.s.gid + s1); csh = 1; crow = l >> 1; chunk = l & 1;
+      d0 = HS_GID + crow * 32;
+    } else if (l < 26) {
+      l -= 24;
+      cbase = (const char*)(a.frame + plane); csh = 0; crow = l;
+      d0 = HS_FRAME + crow * 16;
+    } else if (l < 28) {
+      l -= 26;
+      cbase = (const char*)(a.s.cls + s1); csh = 0; crow = l;
+      d0 = HS_CLS + crow * 16;
+    }
+    cbase += chunk * 16;
+    cdst = (uint32_t)__cvta_generic_to_shared(ring) + d0 + chunk * 16;
+  }
+  // copy tile (t, ty_, tx_) of this warp into ring stage `sidx`; rows past
+  // the frame and tiles past the end are zero-filled
+  auto copy_tile = [&](int t, int ty_, int tx_, int sidx) {
+    __syncwarp();  // the stage's previous tile has been read by every lane
+    if (lane < 28) {
+      const int y = ty_ * 2 + crow;
+      const bool ok = t < a.n_tiles && y < H;
+      const size_t pix = ok ? (size_t)y * W + (size_t)tx_ * 16 : 0;
+      cp_async16(cdst + sidx * HOT_STAGE_BYTES, cbase + (pix << csh),
+                 ok ? 16u : 0u);
+    }
+    cp_async_commit();
+  };
+  auto advance = [&](int& ty_, int& tx_) {
+    ty_ += dty;
+    tx_ += dtx;
+    if (tx_ >= a.tiles_x) {
+      tx_ -= a.tiles_x;
+      ty_ += 1;
+    }
+  };
+
+  int ty = t_first / a.tiles_x, tx = t_first - ty * a.tiles_x;  // front cursor
+  int tf = t_first;
+  int cty = ty, ctx = tx, ct = t_first;                          // copy cursor
+  HotIn nxt;
+  if (PIPE) {
+    // the pending pass wrote through other lanes than the ones that copy
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < HOT_NS - 1; ++j) {
+      copy_tile(ct, cty, ctx, j);
+      ct += step;
+      advance(cty, ctx);
+    }
+    cp_async_wait<HOT_NS - 2>();
+    __syncwarp();
+    nxt = front(tf, ty, tx, ring);
+    tf += step;
+    advance(ty, tx);
+  }
+  for (int it = 0; it < n_it; ++it) {
+    HotIn in;
+    if (PIPE) {
+      copy_tile(ct, cty, ctx, (it + HOT_NS - 1) % HOT_NS);
+      ct += step;
+      advance(cty, ctx);
+      in = nxt;
+      if (it + 1 < n_it) {
+        cp_async_wait<HOT_NS - 2>();
+        __syncwarp();
+        nxt = front(tf, ty, tx, ring + ((it + 1) % HOT_NS) * HOT_STAGE_BYTES);
+        tf += step;
+        advance(ty, tx);
+      }
+    } else {
+      in = front(tf, ty, tx, nullptr);
+      tf += step;
+      advance(ty, tx);
+    }
+
+    // ---- back half: the loaded values and the (cheap) gates again
+    const bool valid = (in.pk >> 15) & 1u;
+    const uint32_t p = in.p;
+    const uint32_t o = plane + p;
+    const int vb = in.pk & 0xFF;
+    const int cls = (in.pk >> 8) & 3u;
+    const int gid = in.pk >> 16;
+    const uint32_t dyn = in.dyn, sk = in.sk;
+    const uint32_t meta = in.mq & 0xFFFFu;
+    const uint32_t q16 = in.mq >> 16;
+    const float2 m0 = in.m0, m1 = in.m1;
     const bool member = valid && G > 0 && gid != (int)UNGROUPED;
     const int gidx = member ? c * G + gid : 0;
     const int dv = abs(vb - (int)(dyn & 0xFF));
@@ -240,10 +462,9 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
     const bool copy = waking && !changed && !on_lat;
     const bool ev = valid && !skip && !copy;
 
-    // ---- level codes, the group test from shared memory, round 2
-    const uint32_t c0 = (meta >> 4) & 3u, c1 = (meta >> 6) & 3u,
-                   c2 = (meta >> 8) & 3u;
-    const uint32_t r0 = (meta >> 10) & 7u, r1 = meta >> 13;
+    // ---- level codes, the group test from shared memory
+    const uint32_t c0 = (meta >> 4) & 3u, c1 = (meta >> 6) & 3u;
+    const uint32_t r0 = (meta >> 10) & 7u, r1 = (meta >> 13) & 7u;
     const uint32_t top = (c0 == L_GROUP && !grouping) ? c1 : c0;
     const bool gtop = top == L_GROUP && member;
     const float vf = (float)vb;
@@ -259,18 +480,7 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
     }
     const int ghit = (grouping && member) ? fmatch(vf, gm, gthr) : 0;
     const bool chp_hit = chp_on && !changed;
-    // the modes are needed unless the confidence reads the group and the
-    // walk stops at the group level (or the probe) before any mode level
-    const bool need =
-        ev && !(gtop && (chp_hit || (c0 == L_GROUP && ghit == 1)));
     T* const rec = mix_s + o * R;  // this plane-pixel's mixture record
-    uint32_t q16 = 0u;
-    float2 m0 = make_float2(0.0f, 1.0f), m1 = m0;
-    if (ev) q16 = __ldcg(tq + ((size_t)t * 256 + vb) * 32);
-    if (need) {
-      m0 = *reinterpret_cast<const float2*>(rec + 2 * r0);
-      m1 = *reinterpret_cast<const float2*>(rec + 2 * r1);
-    }
 
     // ---- evaluation (kernels_numba.py:239-359) in fp32; a decision whose
     // fp32 operands lie inside the filter margin defers the plane-pixel
@@ -381,7 +591,11 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
                 ((uint32_t)(active + 1) << 10) | (clock << 16);
       if (fast) {
         a.s.streak[o] = skn;
-        atomicAdd(a.s.hits + (plane * 5 + (uint32_t)active * P + p), 1u);
+        // one dense RED per plane-pixel: a byte per level below GMM
+        if (hitq != nullptr && active < L_GMM)
+          atomicAdd(hitq + o, 1u << (8 * active));
+        else
+          atomicAdd(a.s.hits + (plane * 5 + (uint32_t)active * P + p), 1u);
         if (active == L_MEAN)
           rec[2 * r0] = (float)((1.0 - rho) * (double)m0.x + rho * (double)vb);
       }

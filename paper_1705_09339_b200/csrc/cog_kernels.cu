@@ -56,9 +56,17 @@ __host__ __device__ inline int acc_fg(int d) { return 7 * d; }
 __host__ __device__ inline int acc_grp(int d, int G, int c, int g) {
   return 7 * d + 1 + (c * G + g) * 6;
 }
-__host__ __device__ inline int acc_words(int d, int G) {
+// last word: nonzero when this frame's pass cleared the packed hit bytes
+// (cog_state.hitq) of every plane-pixel -- reset, reorder or fold
+__host__ __device__ inline int acc_flag(int d, int G) {
   return 7 * d + 1 + 6 * d * G;
 }
+__host__ __device__ inline int acc_words(int d, int G) {
+  return 7 * d + 2 + 6 * d * G;
+}
+// frames the packed hit bytes may collect before they are folded into the
+// wide counters (a byte holds 255)
+constexpr uint32_t HITQ_FOLD_AGE = 250;
 // per (c, g): 0 hit count, 1 sum v over hits, 2 conf hi, 3 conf lo,
 //             4 sum v over all members, 5 member count
 constexpr int CONF_SPLIT = 26;  // conf fixed point: q = floor(conf * 2^52)
@@ -143,6 +151,7 @@ struct PlaneRef {
   uint32_t* dyn;
   uint32_t* streak;
   uint32_t* hits;
+  uint32_t* hitq;      // packed hit bytes of the float32 hot pass, or null
   const float* table;  // this plane's prior, reference layout [P][256]
   const float* peak;
   size_t P;
@@ -162,6 +171,7 @@ __device__ __forceinline__ PlaneRef<T> plane_ref(const StepArgs& a, int s,
   r.dyn = a.s.dyn + sc * P;
   r.streak = a.s.streak + sc * P;
   r.hits = a.s.hits + sc * 5 * P;
+  r.hitq = a.s.hitq ? a.s.hitq + sc * P : nullptr;
   r.table = a.s.table + sc * P * 256;
   r.peak = a.s.peak + sc * P;
   r.P = P;
@@ -229,6 +239,7 @@ __device__ __noinline__ void cold_reset(PlaneRef<T> r, size_t p,
   r.streak[p] = 0;
 #pragma unroll
   for (int l = 0; l < 5; ++l) r.hits[l * r.P + p] = 0;
+  if (r.hitq) r.hitq[p] = 0u;
 }
 
 // Level reorder of one plane-pixel (cascade.py:393-417)
@@ -246,6 +257,7 @@ __device__ __noinline__ void cold_reorder(PlaneRef<T> r, size_t p,
     nm[j] = __longlong_as_double(0x7ff0000000000000ll);     // -(-inf)
     if (code[j] >= 0) {
       nh[j] = -(long long)r.hits[(size_t)code[j] * r.P + p];
+      if (r.hitq && code[j] < 4) nh[j] -= (r.hitq[p] >> (8 * code[j])) & 0xFFu;
       double lmu = group_mu;
       if (code[j] != L_GROUP) {
         int k = meta_ref(meta, code[j] == L_MEAN ? 0 : 1);
@@ -272,6 +284,21 @@ __device__ __noinline__ void cold_reorder(PlaneRef<T> r, size_t p,
   r.meta[p] = (uint16_t)meta_with_mids(meta, out[0], out[1], out[2]);
 #pragma unroll
   for (int l = 0; l < 5; ++l) r.hits[l * r.P + p] = 0;
+  if (r.hitq) r.hitq[p] = 0u;
+}
+
+// the float32 hot pass's packed hit bytes folded into the wide counters
+// (before a byte can wrap: finalize_stream's frame count)
+template <typename T>
+__device__ __forceinline__ void cold_fold_hits(PlaneRef<T> r, size_t p) {
+  const uint32_t q = r.hitq[p];
+  if (!q) return;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const uint32_t b = (q >> (8 * l)) & 0xFFu;
+    if (b) r.hits[l * r.P + p] += b;
+  }
+  r.hitq[p] = 0u;
 }
 
 // MEANVAR level hit: mean+variance update of mode rs, re-sort, remap refs
@@ -667,9 +694,10 @@ __device__ void finalize_stream(const StepArgs& a, int s,
                                 uint32_t* sync) {
   const int d = a.g.depth, G = a.g.n_groups;
   const cog_params& q = a.q;
-  __shared__ int s_fired;
+  __shared__ int s_fired, s_cleared;
   __shared__ long long s_tot[7 * MAXD + 1];
   __syncthreads();
+  if (threadIdx.x == 0) s_cleared = __ldcg(acc + acc_flag(d, G)) != 0ull;
   for (int i = threadIdx.x; i <= 7 * d; i += blockDim.x)
     s_tot[i] = (long long)__ldcg(acc + i);
   __syncthreads();
@@ -732,7 +760,13 @@ __device__ void finalize_stream(const StepArgs& a, int s,
   const int words = acc_words(d, G);
   for (int i = threadIdx.x; i < words; i += blockDim.x) acc[i] = 0ull;
   if (threadIdx.x == 0) {
-    sync[1] = fired ? 1u : 0u;  // pending reset for the next frame
+    // bit 0: pending reset for the next frame; bits 8..15: frames counted
+    // into the packed hit bytes (hitq) since they were last cleared -- by
+    // this frame's reset / reorder / fold (hot_pending), after which this
+    // frame's own hits have been counted
+    const uint32_t age = sync[1] >> 8;
+    const uint32_t na = s_cleared ? 1u : (age < 0xFFFFu ? age + 1u : age);
+    sync[1] = (fired ? 1u : 0u) | (na << 8);
     sync[0] = 0u;               // done counter
     sync[2] = 0u;               // tile counter
     sync[3] = 0u;               // worklist length
@@ -1792,9 +1826,13 @@ __global__ void __launch_bounds__(256) pending_kernel(const StepArgs a) {
 
 // clears the pending flag after pending_kernel (separate launch: every CTA
 // of pending_kernel must have read the flag first)
-__global__ void clear_pending_kernel(uint32_t* sync, int streams) {
+__global__ void clear_pending_kernel(uint32_t* sync, int streams,
+                                     int reorder_now) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < streams) sync[(size_t)s * 4 + 1] = 0u;
+  if (s >= streams) return;
+  // a reset or a reorder cleared the packed hit bytes too: their age restarts
+  const uint32_t v = sync[(size_t)s * 4 + 1];
+  if (reorder_now || (v & 1u)) sync[(size_t)s * 4 + 1] = 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -2027,6 +2065,7 @@ __global__ void __launch_bounds__(128) warmup_kernel(const WarmArgs a) {
   a.s.streak[pi] = 0u;
 #pragma unroll
   for (int l = 0; l < 5; ++l) a.s.hits[((size_t)c * 5 + l) * P + p] = 0u;
+  if (a.s.hitq) a.s.hitq[pi] = 0u;
 }
 
 __global__ void set_levels_kernel(cog_geom g, uint16_t* meta,
@@ -2103,7 +2142,10 @@ __global__ void export_kernel(cog_geom g, cog_state s, cog_ref_state o) {
     o.waking[i] = (uint8_t)dyn_waking(dy);
     o.clock[i] = dyn_clock(dy);
     o.streak[i] = s.streak[i];
-    for (int l = 0; l < 5; ++l) o.hits[i * 5 + l] = s.hits[(c * 5 + l) * P + p];
+    const uint32_t hq = s.hitq ? s.hitq[i] : 0u;
+    for (int l = 0; l < 5; ++l)
+      o.hits[i * 5 + l] = (long long)s.hits[(c * 5 + l) * P + p] +
+                          (l < 4 ? (long long)((hq >> (8 * l)) & 0xFFu) : 0ll);
   }
 }
 
@@ -2135,6 +2177,7 @@ __global__ void import_kernel(cog_geom g, cog_state s, cog_ref_state in) {
       s.hits[(c * 5 + l) * P + p] =
           (uint32_t)(h < 0 ? 0 : (h > 0xffffffffll ? 0xffffffffll : h));
     }
+    if (s.hitq) s.hitq[i] = 0u;
   }
 }
 
@@ -2473,13 +2516,13 @@ int launch_fast(const StepArgs& a, cudaStream_t st) {
   return launch_fast_k<8, 3>(a, st);
 }
 
-template <int KMAX, int D, int ST, int FL>
+template <int KMAX, int D, int ST, int FL, bool PIPE>
 int launch_hot_k(const StepArgs& a, cudaStream_t st) {
-  auto fn = hot_kernel<KMAX, D, ST, FL>;
+  auto fn = hot_kernel<KMAX, D, ST, FL, PIPE>;
   // the group sums and constants move to global memory when they would
   // not fit comfortably (hundreds of groups): any group count runs
   const bool big = hot_smem_bytes(a.g.depth, a.g.n_groups, false) > 24 * 1024;
-  const size_t smem = hot_smem_bytes(a.g.depth, a.g.n_groups, big);
+  const size_t smem = hot_smem_bytes(a.g.depth, a.g.n_groups, big, PIPE);
   if (smem > SMEM_CAP) return COG_EUNSUPPORTED;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2511,9 +2554,17 @@ int launch_hot_cfg(const StepArgs& a, cudaStream_t st) {
                  (a.q.chp_on ? HF_CHP : 0) |
                  (a.q.rate_scaling_on ? HF_RATE : 0) |
                  (a.q.literal_conf ? HF_LITERAL : 0);
-  if (a.g.stride == 2 && fl == HF_DEFAULT)
-    return launch_hot_k<KMAX, D, 2, HF_DEFAULT>(a, st);
-  return launch_hot_k<KMAX, D, 0, -1>(a, st);
+  if (a.g.stride == 2 && fl == HF_DEFAULT) {
+    // the pipelined variant copies 16-byte chunks of 16-pixel rows: every
+    // row of every round-1 array must start on a 16-byte boundary
+    const uintptr_t bases = (uintptr_t)a.frame | (uintptr_t)a.s.dyn |
+                            (uintptr_t)a.s.streak | (uintptr_t)a.s.meta |
+                            (uintptr_t)a.s.gid | (uintptr_t)a.s.cls;
+    if (a.g.width % 16 == 0 && (bases & 15) == 0)
+      return launch_hot_k<KMAX, D, 2, HF_DEFAULT, true>(a, st);
+    return launch_hot_k<KMAX, D, 2, HF_DEFAULT, false>(a, st);
+  }
+  return launch_hot_k<KMAX, D, 0, -1, false>(a, st);
 }
 
 int launch_hotpass(const StepArgs& a, cudaStream_t st) {
@@ -2884,7 +2935,7 @@ int cog_apply_pending(const cog_geom* geom, const cog_params* prm,
   rc = launch_status();
   if (rc) return rc;
   clear_pending_kernel<<<(geom->streams + 127) / 128, 128, 0, s>>>(
-      st->sync, geom->streams);
+      st->sync, geom->streams, reorder_now);
   return launch_status();
 }
 

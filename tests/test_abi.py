@@ -41,7 +41,7 @@ def test_binding_covers_every_declared_symbol():
 def test_host_only_calls():
     lib = _lib.load()
     assert b"sm_100a" in lib.cog_version()
-    assert lib.cog_accum_words(3, 2) == 7 * 3 + 1 + 6 * 3 * 2
+    assert lib.cog_accum_words(3, 2) == 7 * 3 + 2 + 6 * 3 * 2
     assert lib.cog_deepq_slots(3, 1000) == 3000
     # argument validation happens before any CUDA call
     assert lib.cog_step(None, None, None, None, None, None, None, None, 0, 0,

@@ -278,3 +278,30 @@ def test_baseline_config_full_size_f32_vs_oracle(cid, n_run, monkeypatch):
         for k in range(1, 7):  # chp, group, mean, meanvar, gmm, skipped
             assert abs(got[k] - int(row[k])) <= max(2, npp // 1000), (t, k)
     assert agree / total >= 0.9999, (cid, agree, total)
+
+
+@pytest.mark.parametrize("w,h", [(48, 32), (40, 30)])
+def test_f32_hits_equal_kind_counts_across_folds(w, h):
+    """The float32 hot pass counts its hits in packed bytes (cog_state.hitq)
+    that are folded into the wide counters before a byte can wrap: over 600
+    frames with the level window never restarting, `hits` must equal the
+    per-level count of the kinds the engine reported, frame by frame
+    (kernels_numba.py:233,350).  48 wide runs the pipelined hot kernel, 40
+    the direct one."""
+    from paper_1705_09339_b200 import synth
+    from paper_1705_09339_b200.config import EngineConfig
+    n_train, n_run = 30, 600
+    spec = synth.small_spec(2, w, h, n_train + n_run, n_train)
+    frames = synth.Scene(spec).frames(0, n_train + n_run)
+    cfg = EngineConfig(k_max=3, color=True, state_dtype="float32",
+                       reorder_interval=100000, illumination_fraction=1.0)
+    eng = _train(frames[:n_train], cfg)
+    want = np.zeros((3, h * w, 5), dtype=np.int64)
+    for t in range(n_run):
+        eng.process_frame(frames[n_train + t])
+        kinds = eng.last_kinds
+        for lv in range(5):
+            want[:, :, lv] += kinds == lv
+        if t in (0, 249, 250, 251, 255, 256, 499, 500, 501, n_run - 1):
+            assert np.array_equal(eng.hits, want), t
+    assert want[:, :, :4].max() > 255  # a byte would have wrapped

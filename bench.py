@@ -229,15 +229,129 @@ def cpu_baseline(frames, eng, cfg, rows, seconds, min_frames):
     return oe.n_pix * done / dt, dt, done
 
 
+REF_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                       "oracle", "_ref")
+
+
+def real_reference_available():
+    """The unmodified reference package installed under oracle/_ref by
+    __graft_entry__.build() (git-ignored; it travels with the snapshot),
+    plus numba for its default backend."""
+    if not os.path.isdir(os.path.join(REF_DIR, "cogbg")):
+        return False
+    try:
+        import numba  # noqa: F401
+    except ImportError:
+        return False
+    return True
+
+
+_REF_BARRIER = None
+
+
+def _ref_init(barrier):
+    global _REF_BARRIER
+    _REF_BARRIER = barrier
+
+
+def _ref_worker(job):
+    """One host process of the real-reference arm: the reference's own
+    train_engine / process_frame (cogbg, numba backend) on one row band."""
+    train, run, k_max, warmup = job
+    barrier = _REF_BARRIER
+    sys.path.insert(0, REF_DIR)
+    from cogbg.config import EngineConfig as RefConfig
+    from cogbg.frame_io import Frame, FramePlane
+    from cogbg.training import train_engine as ref_train
+
+    def frames_of(arr, base):
+        return [Frame(index=base + i,
+                      planes=[FramePlane(c, arr[i, c])
+                              for c in range(arr.shape[1])])
+                for i in range(arr.shape[0])]
+    cfg = RefConfig(k_max=k_max, color=True, training_frames=train.shape[0])
+    t0 = time.perf_counter()
+    eng = ref_train(frames_of(train, 0), cfg)
+    t_train = time.perf_counter() - t0
+    fr = frames_of(run, train.shape[0])
+    for f in fr[:warmup]:
+        eng.process_frame(f)          # includes the numba compile
+    barrier.wait()
+    t0 = time.perf_counter()
+    for f in fr[warmup:]:
+        eng.process_frame(f)
+    dt = time.perf_counter() - t0
+    return dt, t_train, eng.n_pix
+
+
+def run_real_reference(args, world):
+    """--impl reference with the REAL reference (oracle/_ref/cogbg): its
+    numba kernels are serial, so every host core runs its own engine on a
+    disjoint band of rows of the same frames (as a user of the reference
+    would spread a stream over processes); value = all bands' pixel-frames
+    over the slowest band's time."""
+    import multiprocessing as mp
+    from paper_1705_09339_b200 import synth
+    cid = {"c2": 2, "c3": 3, "c4": 4, "c5": 5}[args.workload]
+    spec = synth.CONFIGS[cid].for_stream(0)
+    cores = len(os.sched_getaffinity(0))
+    n_train = spec.training
+    gen = max(1, min(16, cores))
+    scene = synth.Scene(spec)
+    train = scene.frames(0, n_train, gen)
+    run = scene.frames(n_train, n_train + args.warmup + args.steps, gen)
+    # bounded sample: rows_per even rows per core (stride-aligned bands)
+    rows_per = max(2, min(16, (spec.height // cores) & ~1))
+    nb = min(cores, spec.height // rows_per)
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(nb)
+    jobs = [(np.ascontiguousarray(train[:, :, b * rows_per:(b + 1) * rows_per]),
+             np.ascontiguousarray(run[:, :, b * rows_per:(b + 1) * rows_per]),
+             spec.k_max, args.warmup) for b in range(nb)]
+    with ctx.Pool(nb, initializer=_ref_init, initargs=(barrier,)) as pool:
+        res = pool.map(_ref_worker, jobs, chunksize=1)
+    total = max(r[0] for r in res)
+    pix = sum(r[2] for r in res)
+    value = pix * args.steps / total
+    band = (f" (rows 0-{nb * rows_per - 1} of the {spec.width}x{spec.height} "
+            f"frame, {nb} bands of {rows_per} rows)")
+    line = {
+        "metric": METRIC, "value": value, "unit": "pixel-frames/s",
+        "impl": "reference", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong" if cid == 4 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded BASELINE generator)",
+        "config": {"workload": f"{args.workload.upper()} "
+                               f"{spec.width}x{spec.height}x3 K={spec.k_max} "
+                               f"N={n_train}{band}",
+                   "frames": f"post-training frames {n_train}.."},
+        "cpu_baseline": {"value": value, "unit": "pixel-frames/s",
+                         "cores": nb, "kind": "reference",
+                         "sample": f"{args.steps} frames after {args.warmup} "
+                                   f"warm-up frames{band}; the unmodified "
+                                   f"reference (cogbg, numba backend), one "
+                                   f"process per core; its own training "
+                                   f"{max(r[1] for r in res):.1f}s excluded"},
+        "e2e": {"value": value, "unit": "pixel-frames/s",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_reference(args):
-    """--impl reference: the reference's CPU path (the oracle port of its
-    numba kernels, all host threads) on the same workload; rank 0 only.
-    c4 runs a 270-row band (1/8) of the 4K frame: the full frame needs
-    ~100 GB of host RAM in the reference's layout."""
+    """--impl reference: the reference's CPU path on the same workload; rank
+    0 only.  The real reference (oracle/_ref, see run_real_reference) when it
+    is installed; else the oracle port of its numba kernels on all host
+    threads.  c4 runs a band of the 4K frame: the full frame needs ~100 GB
+    of host RAM in the reference's layout."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return 0
+    if real_reference_available() and not args.port:
+        return run_real_reference(args, world)
     from oracle import oracle as orc
     from paper_1705_09339_b200 import synth
     from paper_1705_09339_b200.config import EngineConfig
@@ -533,6 +647,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="minimum CPU time of the cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--port", action="store_true",
+                    help="--impl reference: time the oracle port even when "
+                         "the real reference is installed (oracle/_ref)")
     ap.add_argument("--variant", default="auto",
                     help="step kernel (engine.kernel_variant; A/B tooling)")
     ap.add_argument("--out", default="")

@@ -263,6 +263,27 @@ int cog_kmeans_assign(const double *points, int64_t n, const double *centers,
                       int32_t k, int64_t *label, uint32_t *changed,
                       void *stream);
 
+/* The grouping's axis-0 reductions (cogbg/grouping.py:100-161: the k-means
+ * centre update `pts[label == j].mean(axis=0)`, standardise's mean / std,
+ * the sigma-band's per-cluster mean / std / ptp).  numpy adds the rows of a
+ * C-contiguous (n, dims) f64 array one after another, so these are
+ * sequential binary64 sums in index order; this reproduces them bit for bit.
+ * For chain (j, f), j < k, f < dims:  out[j * dims + f] = sum, over the rows
+ * i with label[i] == j in index order (label NULL: every row, k = 1), of
+ * x[i][f] (square = 0) or (x[i][f] - shift[j * dims + f])^2 (square = 1);
+ * minmax[2 * chain], [2 * chain + 1] = min / max of x over those rows (or
+ * NULL); count[j] = rows with label j (or NULL).  All device pointers. */
+int cog_seq_sums(const double *x, int64_t n, int32_t dims, const int64_t *label,
+                 int32_t k, const double *shift, int32_t square, double *out,
+                 double *minmax, int64_t *count, void *stream);
+
+/* One farthest-point seeding step (cogbg/grouping.py:100-112): far[i] =
+ * |points[i] - centre|^2 (first != 0) or min(far[i], ...), points f64[n][2],
+ * centre f64[2] on the HOST; best u64[2] on the device receives the bit
+ * pattern of max(far) and np.argmax(far), the lowest index holding it. */
+int cog_far_step(const double *points, int64_t n, const double *centre,
+                 int32_t first, double *far, uint64_t *best, void *stream);
+
 /* Confusion counts of predicted vs truth masks u8[n] (evaluation.
  * confusion_counts, cogbg/evaluation.py:72-89): truth 0 = background,
  * 255 = foreground, anything else excluded; predicted foreground = 255.

@@ -136,6 +136,11 @@ _SIGS = {
     "cog_import_state": (ctypes.c_int, [_P, _P, _P, _P]),
     "cog_step_host": (ctypes.c_int, [_P] * 11 + [ctypes.c_int64,
                                                 ctypes.c_int32] + [_P] * 5),
+    "cog_seq_sums": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int32, _P,
+                                    ctypes.c_int32, _P, ctypes.c_int32, _P,
+                                    _P, _P, _P]),
+    "cog_far_step": (ctypes.c_int, [_P, ctypes.c_int64, _P, ctypes.c_int32,
+                                    _P, _P, _P]),
     "cog_confusion": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P, _P]),
     "cog_pool_sums": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32,
                                      ctypes.c_int64, _P, ctypes.c_int32,

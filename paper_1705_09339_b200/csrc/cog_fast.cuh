@@ -46,7 +46,8 @@ struct FastConst {
   float ct_margin[3];  // |conf - ct| below this -> exact path, per class
   int eps_i;         // changed  <=>  |v - chp| > eps_i
   int sat;           // saturation_frames (clamped to int)
-  int big;           // hot_kernel: group sums / constants in global memory
+  int P;             // hot_kernel: pixels per plane (height * width)
+  int wpad;          // hot_kernel: words of a warp's partial slice in shared
 };
 
 FastConst make_fast_const(const cog_params& q) {

@@ -86,20 +86,43 @@ __device__ __align__(16) uint8_t g_walk[64 * 64];
 #ifndef HOT_NS
 #define HOT_NS 4
 #endif
-constexpr int HOT_STAGE_BYTES = 448;
+#ifndef HOT_PIPE
+#define HOT_PIPE 1  // build-time A/B switch (tools/gpu_ab_build.sh)
+#endif
+constexpr int HOT_STAGE_BYTES = 592;
 constexpr int HS_DYN = 0, HS_STREAK = 128, HS_META = 256, HS_GID = 320,
-              HS_FRAME = 384, HS_CLS = 416;
+              HS_FRAME = 384, HS_CLS = 416,
+              HS_PIX = 448,  // u32[32]: each lane's pixel index, ~0 = invalid
+              HS_TILE = 576; // u32: the tile's index
 
+// shared memory of one CTA, fixed-size parts first (compile-time offsets):
+// the level-walk table, class constants, the tiles' label words, the
+// per-warp worklist buffers, the pipelined ring; then the per-warp partial
+// slices and the group constants, whose size depends on the group count
+__host__ __device__ constexpr int hot_off_cw() { return 64 * 64; }
+__host__ __device__ constexpr int hot_off_ctm() { return hot_off_cw() + 48; }
+__host__ __device__ constexpr int hot_off_lab() { return hot_off_ctm() + 32; }
+__host__ __device__ constexpr int hot_off_qc(int d) {
+  return hot_off_lab() + ((2 * d * HOT_TPB * 4 + 15) & ~15);
+}
+__host__ __device__ constexpr int hot_off_qr(int d) {
+  return hot_off_qc(d) + d * HOT_TPB * HOT_QCAP_BYTES / 2;
+}
+__host__ __device__ constexpr int hot_off_ring(int d) {
+  return hot_off_qr(d) + d * HOT_TPB * HOT_QCAP_BYTES / 2;
+}
+__host__ __device__ constexpr int hot_off_var(int d, bool pipe) {
+  return hot_off_ring(d) + (pipe ? d * HOT_TPB * HOT_NS * HOT_STAGE_BYTES : 0);
+}
+// `big`: the group sums and constants do not fit (hundreds of groups) and
+// live in global memory instead
 __host__ __device__ inline size_t hot_smem_bytes(int d, int G, bool big,
                                                  bool pipe = false) {
   const int g = big ? 0 : G;
   const int warps = d * HOT_TPB;
   const size_t wpad = ((size_t)acc_words(d, g) + 1) & ~(size_t)1;
-  size_t n = (size_t)warps * wpad * 8 + (size_t)warps * HOT_QCAP_BYTES +
-             64 * 64 + 3 * 32 + (size_t)2 * d * g * 4 +
-             (size_t)2 * warps * 4 + 16;
-  if (pipe) n = ((n + 15) & ~(size_t)15) + (size_t)warps * HOT_NS * HOT_STAGE_BYTES;
-  return n;
+  return (size_t)hot_off_var(d, pipe) + (size_t)warps * wpad * 8 +
+         (size_t)2 * d * g * 4 + 16;
 }
 
 // one plane-pixel's loads, handed from the front half of the tile loop
@@ -108,10 +131,14 @@ __host__ __device__ inline size_t hot_smem_bytes(int d, int G, bool big,
 struct HotIn {
   uint32_t p;     // pixel index (0 for an invalid lane)
   uint32_t dyn, sk;
-  uint32_t mq;    // meta | q16 << 16
-  uint32_t pk;    // v | cls << 8 | valid << 15 | gid << 16
+  uint32_t mf;    // meta | the front half's gates << 16 (HI_*)
+  uint32_t pk;    // v | cls << 8 | gid << 16
+  uint32_t q16;   // hot prior at v (its own register: packing it would
+                  // wait for the load in the front half)
   float2 m0, m1;  // the two referenced modes (mu, var)
 };
+enum : uint32_t { HI_VALID = 1u << 16, HI_SKIP = 1u << 17, HI_COPY = 1u << 18,
+                  HI_GHIT_SHIFT = 19 };  // ghit & 3 at bits 19-20
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src,
                                            uint32_t src_bytes) {
@@ -144,30 +171,36 @@ constexpr int HF_DEFAULT = HF_SAMPLING | HF_GROUPING | HF_CHP | HF_RATE;
 // warp's shared ring, and the front half (gates, prior and mode loads) of
 // tile j + 1 is issued before the back half of tile j runs, so both load
 // rounds overlap a whole tile of evaluation without holding registers
-template <int KMAX, int D, int ST, int FL, bool PIPE>
+template <int KMAX, int D, int ST, int FL, bool PIPE, bool BIG>
 __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB))
     hot_kernel(const __grid_constant__ StepArgs a,
                const __grid_constant__ FastConst k) {
   static_assert(!PIPE || ST == 2, "the pipelined ring is laid out for stride 2");
   using T = float;
   constexpr int R = rec_elems(KMAX), WO = rec_w(KMAX);
-  extern __shared__ unsigned long long h_mem[];
+  extern __shared__ __align__(16) unsigned char h_raw[];
   const int s = blockIdx.y;
   const int G = a.g.n_groups;
   const int H = a.g.height, W = a.g.width;
   const int stride = ST > 0 ? ST : a.g.stride;
   const int cw = ST > 0 ? ST * (32 / (ST * ST) > 0 ? 32 / (ST * ST) : 1) : a.cw;
-  const uint32_t P = (uint32_t)H * (uint32_t)W;
+  const uint32_t P = (uint32_t)k.P;  // H * W (launcher)
   const int words = acc_words(D, G);
-  const bool big = k.big != 0;  // group sums / constants in global memory
+  constexpr bool big = BIG;  // group sums / constants in global memory
   const int sG = big ? 0 : G;
-  const int wpad = (acc_words(D, sG) + 1) & ~1;
+  const int wpad = k.wpad;   // (acc_words(D, sG) + 1) & ~1 (launcher)
   constexpr int NW = D * HOT_TPB;   // warps per CTA
   constexpr int NT = 32 * NW;       // threads per CTA
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  const int c = w % D;              // this warp's plane
-  const int slot = w / D;           // this warp's tile of the CTA's HOT_TPB
+  // read once (volatile: the compiler would otherwise re-read %tid.x, a
+  // slow special-register move, all over the loop instead of keeping it)
+  unsigned tid_x;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid_x));
+  const int lane = tid_x & 31;
+  const int w = tid_x >> 5;
+  // this warp's tile of the CTA's HOT_TPB and its plane (no division)
+  const int slot = (w >= D) + (HOT_TPB > 2 && w >= 2 * D) +
+                   (HOT_TPB > 3 && w >= 3 * D);
+  const int c = w - slot * D;
   const bool sampling = FL < 0 ? a.q.sampling_on != 0 : (FL & HF_SAMPLING) != 0;
   const bool grouping = FL < 0 ? a.q.grouping_on != 0 : (FL & HF_GROUPING) != 0;
   const bool chp_on = FL < 0 ? a.q.chp_on != 0 : (FL & HF_CHP) != 0;
@@ -178,15 +211,17 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
   // per-warp worklist buffers, the level-walk table, the per-class
   // confidence constants, group constants (float), the tiles' per-plane
   // label words (double buffered)
-  unsigned long long* s_wacc = h_mem;                    // [NW][wpad]
-  unsigned long long* s_qc = s_wacc + NW * wpad;         // [NW][HQ_CAP]
-  double* s_qr = (double*)(s_qc + NW * HQ_CAP);          // [NW][HQ_CAP]
-  uint8_t* s_walk = (uint8_t*)(s_qr + NW * HQ_CAP);      // [64 * 64]
-  float4* s_cw = (float4*)(s_walk + 64 * 64);            // [3] wa wb wc 1/(wb+wc)
-  float* s_ctm = (float*)(s_cw + 3);                     // [3] conf margins
-  float* s_gmu = s_ctm + 5;                              // [D*G]
-  float* s_gthr = s_gmu + D * sG;                        // [D*G]
-  unsigned* s_lab = (unsigned*)(s_gthr + D * sG);        // [2][NW]
+  uint8_t* const s_walk = h_raw;                                    // [64 * 64]
+  float4* const s_cw = (float4*)(h_raw + hot_off_cw());             // [3] wa wb wc 1/(wb+wc)
+  float* const s_ctm = (float*)(h_raw + hot_off_ctm());             // [3] conf margins
+  unsigned* const s_lab = (unsigned*)(h_raw + hot_off_lab());       // [2][NW]
+  unsigned long long* const s_qc =
+      (unsigned long long*)(h_raw + hot_off_qc(D));                 // [NW][HQ_CAP]
+  double* const s_qr = (double*)(h_raw + hot_off_qr(D));            // [NW][HQ_CAP]
+  unsigned long long* const s_wacc =
+      (unsigned long long*)(h_raw + hot_off_var(D, PIPE));          // [NW][wpad]
+  float* const s_gmu = (float*)(s_wacc + NW * wpad);                // [D*G]
+  float* const s_gthr = s_gmu + D * sG;                             // [D*G]
   const double* gmu_d = a.s.g_mu + (size_t)s * D * G;
   const double* gvar_d = a.s.g_var + (size_t)s * D * G;
   for (int i = threadIdx.x; i < D * sG; i += NT) {
@@ -266,9 +301,18 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
   // ring stage `st` the copies have filled
   auto front = [&](int t, int ty_, int tx_, const unsigned char* st) -> HotIn {
     HotIn in;
-    const int y = ty_ * stride + lrow, x = tx_ * cw + lcol;
-    const bool valid = lane_ok && t < a.n_tiles && y < H && x < W;
-    const uint32_t p = valid ? (uint32_t)y * (uint32_t)W + (uint32_t)x : 0u;
+    bool valid;
+    uint32_t p;
+    if (PIPE) {
+      p = *reinterpret_cast<const uint32_t*>(st + HS_PIX + lane * 4);
+      t = *reinterpret_cast<const int*>(st + HS_TILE);
+      valid = p != 0xFFFFFFFFu;
+      if (!valid) p = 0u;
+    } else {
+      const int y = ty_ * stride + lrow, x = tx_ * cw + lcol;
+      valid = lane_ok && t < a.n_tiles && y < H && x < W;
+      p = valid ? (uint32_t)y * (uint32_t)W + (uint32_t)x : 0u;
+    }
     const uint32_t o = plane + p;
     int vb, gid, cls;
     uint32_t dyn, meta, sk;
@@ -330,9 +374,10 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
     in.p = p;
     in.dyn = dyn;
     in.sk = sk;
-    in.mq = (meta & 0xFFFFu) | (q16 << 16);
-    in.pk = (uint32_t)vb | ((uint32_t)cls << 8) | ((uint32_t)valid << 15) |
-            ((uint32_t)gid << 16);
+    in.q16 = q16;
+    in.mf = (meta & 0xFFFFu) | (valid ? HI_VALID : 0u) | (skip ? HI_SKIP : 0u) |
+            (copy ? HI_COPY : 0u) | (((uint32_t)ghit & 3u) << HI_GHIT_SHIFT);
+    in.pk = (uint32_t)vb | ((uint32_t)cls << 8) | ((uint32_t)gid << 16);
     return in;
   };
 
@@ -344,9 +389,7 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
   uint32_t cdst = 0;            // shared address of the chunk in stage 0
   unsigned char* ring = nullptr;
   if (PIPE) {
-    const size_t off = (hot_smem_bytes(D, G, big, false) + 15) & ~(size_t)15;
-    ring = reinterpret_cast<unsigned char*>(h_mem) + off +
-           (size_t)w * HOT_NS * HOT_STAGE_BYTES;
+    ring = h_raw + hot_off_ring(D) + w * (HOT_NS * HOT_STAGE_BYTES);
     int l = lane, chunk = 0;
     uint32_t d0 = 0;
     if (l < 8) {
@@ -380,6 +423,17 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
   // the frame and tiles past the end are zero-filled
   auto copy_tile = [&](int t, int ty_, int tx_, int sidx) {
     __syncwarp();  // the stage's previous tile has been read by every lane
+    {
+      // each lane's pixel of this tile and the tile index ride along, so
+      // the front half needs no cursor of its own
+      unsigned char* st = ring + sidx * HOT_STAGE_BYTES;
+      const int y = ty_ * 2 + lrow;
+      const bool v = t < a.n_tiles && y < H;
+      *reinterpret_cast<uint32_t*>(st + HS_PIX + lane * 4) =
+          v ? (uint32_t)y * (uint32_t)W + (uint32_t)(tx_ * 16 + lcol)
+            : 0xFFFFFFFFu;
+      if (lane == 0) *reinterpret_cast<int*>(st + HS_TILE) = t;
+    }
     if (lane < 28) {
       const int y = ty_ * 2 + crow;
       const bool ok = t < a.n_tiles && y < H;
@@ -398,38 +452,34 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
     }
   };
 
-  int ty = t_first / a.tiles_x, tx = t_first - ty * a.tiles_x;  // front cursor
+  // the tile cursor: of the copies when pipelined, else of the front half
+  int ty = t_first / a.tiles_x, tx = t_first - ty * a.tiles_x;
   int tf = t_first;
-  int cty = ty, ctx = tx, ct = t_first;                          // copy cursor
   HotIn nxt;
   if (PIPE) {
     // the pending pass wrote through other lanes than the ones that copy
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < HOT_NS - 1; ++j) {
-      copy_tile(ct, cty, ctx, j);
-      ct += step;
-      advance(cty, ctx);
+      copy_tile(tf, ty, tx, j);
+      tf += step;
+      advance(ty, tx);
     }
     cp_async_wait<HOT_NS - 2>();
     __syncwarp();
-    nxt = front(tf, ty, tx, ring);
-    tf += step;
-    advance(ty, tx);
+    nxt = front(0, 0, 0, ring);
   }
   for (int it = 0; it < n_it; ++it) {
     HotIn in;
     if (PIPE) {
-      copy_tile(ct, cty, ctx, (it + HOT_NS - 1) % HOT_NS);
-      ct += step;
-      advance(cty, ctx);
+      copy_tile(tf, ty, tx, (it + HOT_NS - 1) % HOT_NS);
+      tf += step;
+      advance(ty, tx);
       in = nxt;
       if (it + 1 < n_it) {
         cp_async_wait<HOT_NS - 2>();
         __syncwarp();
-        nxt = front(tf, ty, tx, ring + ((it + 1) % HOT_NS) * HOT_STAGE_BYTES);
-        tf += step;
-        advance(ty, tx);
+        nxt = front(0, 0, 0, ring + ((it + 1) % HOT_NS) * HOT_STAGE_BYTES);
       }
     } else {
       in = front(tf, ty, tx, nullptr);
@@ -437,16 +487,16 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
       advance(ty, tx);
     }
 
-    // ---- back half: the loaded values and the (cheap) gates again
-    const bool valid = (in.pk >> 15) & 1u;
+    // ---- back half: the loaded values and the front half's gates
+    const bool valid = (in.mf & HI_VALID) != 0u;
     const uint32_t p = in.p;
     const uint32_t o = plane + p;
     const int vb = in.pk & 0xFF;
     const int cls = (in.pk >> 8) & 3u;
     const int gid = in.pk >> 16;
     const uint32_t dyn = in.dyn, sk = in.sk;
-    const uint32_t meta = in.mq & 0xFFFFu;
-    const uint32_t q16 = in.mq >> 16;
+    const uint32_t meta = in.mf & 0xFFFFu;
+    const uint32_t q16 = in.q16;
     const float2 m0 = in.m0, m1 = in.m1;
     const bool member = valid && G > 0 && gid != (int)UNGROUPED;
     const int gidx = member ? c * G + gid : 0;
@@ -457,9 +507,8 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
     // ---- sampling gate (kernels_numba.py:189-216): skip, copy, evaluate
     // (after waking on a change the streak restarts)
     const bool asleep = sampling && (dyn >> 16) != 0u;
-    const bool waking = sampling && !asleep && ((dyn >> 9) & 1u);
-    const bool skip = asleep && !changed;
-    const bool copy = waking && !changed && !on_lat;
+    const bool skip = (in.mf & HI_SKIP) != 0u;
+    const bool copy = (in.mf & HI_COPY) != 0u;
     const bool ev = valid && !skip && !copy;
 
     // ---- level codes, the group test from shared memory
@@ -478,7 +527,6 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
         gthr = (float)(a.q.match_lambda * sqrt(gvar_d[gidx]));
       }
     }
-    const int ghit = (grouping && member) ? fmatch(vf, gm, gthr) : 0;
     const bool chp_hit = chp_on && !changed;
     T* const rec = mix_s + o * R;  // this plane-pixel's mixture record
 
@@ -504,7 +552,7 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
                            fabsf(cf_ev - k.ct) <= ct_m);
     // the level tests, then the first decisive one in mid_order (table)
     const uint32_t codes = ((meta >> 4) & 63u) << 6;
-    uint32_t sg = (uint32_t)ghit & 3u;  // 0 miss, 1 hit, 3 undecided
+    uint32_t sg = (in.mf >> HI_GHIT_SHIFT) & 3u;  // 0 miss, 1 hit, 3 undecided
     uint32_t sm0 = (uint32_t)fmatch(vf, m0.x, thr0) & 3u;
     uint32_t sm1 = (uint32_t)fmatch(vf, m1.x, thr1) & 3u;
     auto walk = [&]() {

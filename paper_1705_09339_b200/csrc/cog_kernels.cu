@@ -1403,15 +1403,27 @@ __device__ __forceinline__ float d32_rcp(float x) {
   return r;
 }
 
-// stable descending order by w / sqrt(var); false on a near tie
+// stable descending order by w / sqrt(var); false on a near tie.  The
+// mixture was sorted before the update and an update moves one mode's key,
+// so nearly always the order stands: `same` = every adjacent pair is still
+// in order by more than the margin (inv is the identity, nothing moves)
 template <int KMAX>
 __device__ __forceinline__ bool d32_sort(float (&mu)[KMAX], float (&var)[KMAX],
                                          float (&w)[KMAX], int n,
-                                         int (&inv)[KMAX]) {
+                                         int (&inv)[KMAX], bool& same) {
   float key[KMAX];
 #pragma unroll
   for (int k = 0; k < KMAX; ++k)
     key[k] = k < n ? w[k] * d32_rsqrt(var[k]) : 0.0f;
+  same = true;
+#pragma unroll
+  for (int k = 0; k + 1 < KMAX; ++k)
+    if (k + 1 < n)
+      same &= key[k] - key[k + 1] >
+              1e-5f * fmaxf(fabsf(key[k]), fabsf(key[k + 1])) + 1e-30f;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) inv[k] = k;
+  if (same) return true;
   bool ok = true;
 #pragma unroll
   for (int i = 0; i < KMAX; ++i) {
@@ -1578,8 +1590,18 @@ __device__ __forceinline__ unsigned deep_item_f32(const StepArgs& a, int s,
     }
   }
   int inv[KMAX];
-  if (!d32_sort<KMAX>(mu, var, w, n, inv)) {
+  bool same;
+  if (!d32_sort<KMAX>(mu, var, w, n, inv, same)) {
     ok = false;
+    return 0;
+  }
+  if (same && kindq == DEEP_MEANVAR) {
+    // the order stands: only mode rs changed, the refs stay
+    float2 mv = make_float2(0.0f, 1.0f);
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      if (k == rs) mv = make_float2(mu[k], var[k]);
+    *reinterpret_cast<float2*>(rec_of(pr, p) + 2 * rs) = mv;
     return 0;
   }
   // ---- write back (deep_item's bookkeeping): the whole record
@@ -2225,6 +2247,113 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
+// training: the grouping's axis-0 reductions (grouping.py:100-161).  numpy
+// sums the rows of a C-contiguous (n, dims) array one after another, so the
+// reference's cluster means / deviations are SEQUENTIAL binary64 sums in
+// index order -- not re-associable.  One warp per (label, column) chain:
+// the warp loads 32 rows at a time (coalesced, next chunk in flight), then
+// adds the matching rows' terms in index order (every lane keeps the same
+// accumulator; the loop runs over the matching lanes only).  The chains of
+// all labels and columns run side by side, each at one dependent DADD per
+// member.  term = x (square = 0) or (x - shift[chain])^2 (square = 1).
+// Also the chain's min and max (np.ptp) and the label's member count.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(32)
+    seq_sums_kernel(const double* __restrict__ x, int64_t n, int dims,
+                    const int64_t* __restrict__ label, int k,
+                    const double* __restrict__ shift, int square, double* out,
+                    double* minmax, long long* count) {
+  const int chain = blockIdx.x, j = chain / dims, f = chain - j * dims;
+  const int lane = threadIdx.x;
+  const double sh = shift ? shift[chain] : 0.0;
+  double acc = 0.0;
+  double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+  long long cnt = 0;
+  double t_cur = 0.0, t_nxt = 0.0;
+  bool m_cur = false, m_nxt = false;
+  auto load = [&](int64_t i0, double& t, bool& m) {
+    const int64_t i = i0 + lane;
+    m = i < n && (!label || label[i] == (int64_t)j);
+    t = 0.0;
+    if (m) {
+      const double v = x[i * dims + f];
+      mn = fmin(mn, v);
+      mx = fmax(mx, v);
+      const double dv = v - sh;
+      t = square ? dv * dv : v;
+    }
+  };
+  load(0, t_cur, m_cur);
+  for (int64_t i0 = 0; i0 < n; i0 += 32) {
+    if (i0 + 32 < n) load(i0 + 32, t_nxt, m_nxt);
+    unsigned bal = __ballot_sync(FULL, m_cur);
+    cnt += __popc(bal);
+    while (bal) {
+      const int l = __ffs(bal) - 1;
+      bal &= bal - 1;
+      acc = acc + __shfl_sync(FULL, t_cur, l);
+    }
+    t_cur = t_nxt;
+    m_cur = m_nxt;
+    m_nxt = false;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(FULL, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  }
+  if (lane == 0) {
+    out[chain] = acc;
+    if (minmax) {
+      minmax[2 * chain] = mn;
+      minmax[2 * chain + 1] = mx;
+    }
+    if (count && f == 0) count[j] = cnt;
+  }
+}
+
+// farthest-point seeding step (grouping.py:100-112): far[i] = min(far[i],
+// |pts[i] - c|^2) (first: far[i] = |pts[i] - c|^2), then np.argmax(far) =
+// the lowest index of the largest value, in two passes over `best`
+// (best[0] = max bits of far, best[1] = lowest index holding it; far >= 0,
+// so its bit pattern orders like the value)
+__global__ void __launch_bounds__(256)
+    far_update_kernel(const double* __restrict__ pts, int64_t n, double c0,
+                      double c1, int first, double* __restrict__ far,
+                      unsigned long long* best) {
+  unsigned long long m = 0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double d0 = pts[2 * i] - c0, d1 = pts[2 * i + 1] - c1;
+    double d = d0 * d0 + d1 * d1;
+    if (!first) d = fmin(far[i], d);  // np.minimum(far, d)
+    far[i] = d;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    m = b > m ? b : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(FULL, m, o);
+    m = t > m ? t : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(best, m);
+}
+
+__global__ void __launch_bounds__(256)
+    far_argmax_kernel(const double* __restrict__ far, int64_t n,
+                      unsigned long long* best) {
+  const unsigned long long want = best[0];
+  unsigned long long m = ~0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if ((unsigned long long)__double_as_longlong(far[i]) == want)
+      m = (unsigned long long)i < m ? (unsigned long long)i : m;
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(FULL, m, o);
+    m = t < m ? t : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m != ~0ull) atomicMin(best + 1, m);
+}
+
+// ---------------------------------------------------------------------------
 // training: pooled group statistics (grouping.py:189-192) for pools too big
 // for numpy's in-memory expression: per (group, plane) the exact integer sums
 // of x and x^2 over every training frame of every member pixel.  One thread
@@ -2516,12 +2645,10 @@ int launch_fast(const StepArgs& a, cudaStream_t st) {
   return launch_fast_k<8, 3>(a, st);
 }
 
-template <int KMAX, int D, int ST, int FL, bool PIPE>
+template <int KMAX, int D, int ST, int FL, bool PIPE, bool BIG>
 int launch_hot_k(const StepArgs& a, cudaStream_t st) {
-  auto fn = hot_kernel<KMAX, D, ST, FL, PIPE>;
-  // the group sums and constants move to global memory when they would
-  // not fit comfortably (hundreds of groups): any group count runs
-  const bool big = hot_smem_bytes(a.g.depth, a.g.n_groups, false) > 24 * 1024;
+  auto fn = hot_kernel<KMAX, D, ST, FL, PIPE, BIG>;
+  constexpr bool big = BIG;
   const size_t smem = hot_smem_bytes(a.g.depth, a.g.n_groups, big, PIPE);
   if (smem > SMEM_CAP) return COG_EUNSUPPORTED;
   if (smem > 48 * 1024)
@@ -2540,9 +2667,19 @@ int launch_hot_k(const StepArgs& a, cudaStream_t st) {
   const int need = (a.n_tiles + HOT_TPB - 1) / HOT_TPB;
   const int gx = need < per_stream ? need : per_stream;
   FastConst k = make_fast_const(a.q);
-  k.big = big ? 1 : 0;
+  k.P = a.g.height * a.g.width;
+  k.wpad = (acc_words(a.g.depth, big ? 0 : a.g.n_groups) + 1) & ~1;
   fn<<<dim3(gx < 1 ? 1 : gx, a.g.streams), threads, smem, st>>>(a, k);
   return launch_status();
+}
+
+// the group sums and constants move to global memory when they would not
+// fit comfortably in shared memory (hundreds of groups): any group count runs
+template <int KMAX, int D, int ST, int FL, bool PIPE>
+int launch_hot_b(const StepArgs& a, cudaStream_t st) {
+  if (hot_smem_bytes(a.g.depth, a.g.n_groups, false, false) > 24 * 1024)
+    return launch_hot_k<KMAX, D, ST, FL, PIPE, true>(a, st);
+  return launch_hot_k<KMAX, D, ST, FL, PIPE, false>(a, st);
 }
 
 // the production configuration (stride 2, the reference's default feature
@@ -2560,11 +2697,11 @@ int launch_hot_cfg(const StepArgs& a, cudaStream_t st) {
     const uintptr_t bases = (uintptr_t)a.frame | (uintptr_t)a.s.dyn |
                             (uintptr_t)a.s.streak | (uintptr_t)a.s.meta |
                             (uintptr_t)a.s.gid | (uintptr_t)a.s.cls;
-    if (a.g.width % 16 == 0 && (bases & 15) == 0)
-      return launch_hot_k<KMAX, D, 2, HF_DEFAULT, true>(a, st);
-    return launch_hot_k<KMAX, D, 2, HF_DEFAULT, false>(a, st);
+    if (HOT_PIPE && a.g.width % 16 == 0 && (bases & 15) == 0)
+      return launch_hot_b<KMAX, D, 2, HF_DEFAULT, true>(a, st);
+    return launch_hot_b<KMAX, D, 2, HF_DEFAULT, false>(a, st);
   }
-  return launch_hot_k<KMAX, D, 0, -1, false>(a, st);
+  return launch_hot_b<KMAX, D, 0, -1, false>(a, st);
 }
 
 int launch_hotpass(const StepArgs& a, cudaStream_t st) {
@@ -2859,6 +2996,35 @@ int cog_kmeans_assign(const double* points, int64_t n, const double* centers,
   if (blocks > cap) blocks = cap;
   kmeans_assign_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
       points, n, centers, k, label, changed);
+  return launch_status();
+}
+
+int cog_seq_sums(const double* x, int64_t n, int32_t dims,
+                 const int64_t* label, int32_t k, const double* shift,
+                 int32_t square, double* out, double* minmax, int64_t* count,
+                 void* stream) {
+  if (!x || !out || n < 0 || dims < 1 || k < 1) return COG_EINVAL;
+  if (square && !shift) return COG_EINVAL;
+  seq_sums_kernel<<<(unsigned)(k * dims), 32, 0, (cudaStream_t)stream>>>(
+      x, n, dims, label, k, shift, square, out, minmax, (long long*)count);
+  return launch_status();
+}
+
+int cog_far_step(const double* points, int64_t n, const double* centre,
+                 int32_t first, double* far, uint64_t* best, void* stream) {
+  if (!points || !centre || !far || !best || n < 1) return COG_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t blocks = (n + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  const unsigned long long init[2] = {0ull, ~0ull};
+  cudaError_t e = cudaMemcpyAsync(best, init, sizeof(init),
+                                  cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return (int)e;
+  far_update_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+      points, n, centre[0], centre[1], first, far, (unsigned long long*)best);
+  far_argmax_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+      far, n, (unsigned long long*)best);
   return launch_status();
 }
 

@@ -1,13 +1,18 @@
-"""Training phase 2: spatio-temporal grouping (host side).
+"""Training phase 2: spatio-temporal grouping.
 
 Algorithm of /root/reference/pkg/src/cogbg/grouping.py:85-208: z-scored
 behaviour features -> seeded farthest-point k-means -> sigma-band trimming
--> pooled per-group, per-plane mode.  The features themselves are produced
-on the GPU by the warm-up kernel (``cog_gmm_warmup``, bit-identical to
-``numpy.var(axis=0)`` of the adaptation series); only the global, discrete
-clustering runs here, in numpy with the reference's exact expressions so the
-group map is identical.  It is training-time work ("gather
-per-pixel features to host, run build_groups").
+-> pooled per-group, per-plane mode.  The features are produced on the GPU
+by the warm-up kernel (``cog_gmm_warmup``, bit-identical to
+``numpy.var(axis=0)`` of the adaptation series).
+
+At scale (>= ``KMEANS_DEVICE_MIN`` pixels) the whole clustering runs on the
+device (``build_groups_device``): the seeding (``cog_far_step``), the
+assignment (``cog_kmeans_assign``), and every axis-0 reduction -- centre
+update, z-score, sigma band -- through ``cog_seq_sums``, which reproduces
+numpy's row-after-row binary64 summation order, so the group map is the
+reference's bit for bit; the elementwise steps are IEEE-exact tensor ops.
+Small frames use the numpy expressions below (the same arithmetic).
 """
 
 from __future__ import annotations
@@ -218,6 +223,128 @@ def _pooled_stats_device(values: np.ndarray, values_dev, gm: "GroupMap",
             gm.var[gi, c] = max((cnt * s2 - s1 * s1) / (cnt * cnt), floor)
 
 
+def _seq_sums(x, label, k, shift=None, minmax=False):
+    """Sequential axis-0 sums per label of the device tensor x (n, dims) f64
+    (cog_seq_sums): returns (sums (k, dims), minmax (k, dims, 2) or None,
+    counts (k,)) as numpy arrays."""
+    import torch
+
+    from . import _lib
+    n, dims = x.shape
+    dev = x.device
+    out = torch.empty((k, dims), dtype=torch.float64, device=dev)
+    mm = torch.empty((k, dims, 2), dtype=torch.float64, device=dev) \
+        if minmax else None
+    cnt = torch.zeros(k, dtype=torch.int64, device=dev)
+    sh = None
+    if shift is not None:
+        sh = torch.from_numpy(np.ascontiguousarray(
+            shift, dtype=np.float64).reshape(k, dims)).to(dev)
+    _lib.check(_lib.load().cog_seq_sums(
+        x.data_ptr(), n, dims,
+        label.data_ptr() if label is not None else None, k,
+        sh.data_ptr() if sh is not None else None, int(sh is not None),
+        out.data_ptr(), mm.data_ptr() if mm is not None else None,
+        cnt.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+        "cog_seq_sums")
+    return (out.cpu().numpy(), mm.cpu().numpy() if mm is not None else None,
+            cnt.cpu().numpy())
+
+
+def build_groups_device(features, w_final, values: np.ndarray,
+                        config: EngineConfig, values_dev=None) -> GroupMap:
+    """build_groups with features (P, 2) / w_final (P,) f64 on the device
+    (tensors, or arrays that are uploaded): the reference's clustering
+    (grouping.py:100-195) step for step, every reduction in numpy's order
+    (module docstring).  Only the group map, the per-group scalars and the
+    compacted member weights come back to the host."""
+    import torch
+
+    from . import _lib
+    lib = _lib.load()
+    n_fr, d, p = values.shape
+    dev = torch.device("cuda", torch.cuda.current_device())
+    f = torch.as_tensor(features).to(dev, torch.float64).contiguous()
+    wf = torch.as_tensor(w_final).to(dev, torch.float64).contiguous()
+    if tuple(f.shape) != (p, 2):
+        raise TrainingError("feature geometry does not match frames")
+    k = config.clusters
+    if p < k:
+        raise ClusteringError(f"{p} pixels cannot form {k} clusters")
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    # ---- standardise (grouping.py:93-97)
+    s1, _, _ = _seq_sums(f, None, 1)
+    mean = s1[0] / p
+    q, _, _ = _seq_sums(f, None, 1, shift=mean)
+    std = np.sqrt(q[0] / p)
+    den = np.where(std > 0, std, 1.0)
+    z = ((f - torch.from_numpy(mean).to(dev))
+         / torch.from_numpy(den).to(dev)).contiguous()
+    # ---- farthest-point seeding (grouping.py:100-112)
+    first = int(np.random.default_rng(config.cluster_seed).integers(p))
+    ctr = np.empty((k, 2))
+    ctr[0] = z[first].cpu().numpy()
+    far = torch.empty(p, dtype=torch.float64, device=dev)
+    best = torch.empty(2, dtype=torch.int64, device=dev)
+    for j in range(1, k):
+        c_prev = np.ascontiguousarray(ctr[j - 1])
+        _lib.check(lib.cog_far_step(z.data_ptr(), p, c_prev.ctypes.data,
+                                    int(j == 1), far.data_ptr(),
+                                    best.data_ptr(), stream), "cog_far_step")
+        ctr[j] = z[int(best[1].item())].cpu().numpy()
+    # ---- k-means (grouping.py:113-126)
+    lab = torch.full((p,), -1, dtype=torch.int64, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    c_dev = torch.empty((k, 2), dtype=torch.float64, device=dev)
+    for _ in range(100):
+        c_dev.copy_(torch.from_numpy(np.ascontiguousarray(ctr)))
+        flag.zero_()
+        _lib.check(lib.cog_kmeans_assign(
+            z.data_ptr(), p, c_dev.data_ptr(), k, lab.data_ptr(),
+            flag.data_ptr(), stream), "cog_kmeans_assign")
+        if int(flag.item()) == 0:
+            break
+        sums, _, cnt = _seq_sums(z, lab, k)
+        for j in range(k):
+            if cnt[j]:
+                ctr[j] = sums[j] / cnt[j]
+    # ---- sigma band on the raw features (grouping.py:142-161)
+    sums, mm, cnt = _seq_sums(f, lab, k, minmax=True)
+    safe = np.maximum(cnt, 1)[:, None]
+    cmean = sums / safe
+    q, _, _ = _seq_sums(f, lab, k, shift=cmean)
+    cstd = config.cluster_threshold * np.sqrt(q / safe)
+    flat = torch.from_numpy((mm[:, :, 1] - mm[:, :, 0]) == 0).to(dev)
+    inside = ((f - torch.from_numpy(cmean).to(dev)[lab]).abs()
+              <= torch.from_numpy(cstd).to(dev)[lab]) | flat[lab]
+    keep = inside.all(dim=1) & torch.from_numpy(cnt >= 2).to(dev)[lab]
+    member = torch.where(keep, lab, torch.full_like(lab, UNGROUPED))
+    cnt2 = torch.bincount(member[member >= 0], minlength=k).cpu().numpy()
+    kept = [j for j in range(k) if cnt2[j] >= 2]
+    g = len(kept)
+    remap = np.full(k + 1, UNGROUPED, dtype=np.int64)   # [-1] -> ungrouped
+    for gi, j in enumerate(kept):
+        remap[j] = gi
+    gid_dev = torch.from_numpy(remap).to(dev)[member]
+    gm = GroupMap(gid_dev.cpu().numpy(), np.zeros((g, d)), np.zeros((g, d)),
+                  np.zeros(g), np.zeros(g, dtype=np.int64))
+    big = []
+    for gi, j in enumerate(kept):
+        gm.member_count[gi] = cnt2[j]
+        # 1-D contiguous mean: numpy's own (pairwise) sum on the compacted,
+        # order-preserved member weights
+        gm.weight[gi] = wf[gid_dev == gi].cpu().numpy().mean()
+        if n_fr * d * int(cnt2[j]) * 8 > _POOL_EXACT_BYTES:
+            big.append(gi)
+        else:
+            gm.mu[gi], gm.var[gi] = _pooled_stats(values, gm.group_id == gi,
+                                                  config.variance_floor)
+    if big:
+        _pooled_stats_device(values, values_dev, gm, big,
+                             config.variance_floor)
+    return gm
+
+
 def _cuda_ok() -> bool:
     try:
         import torch
@@ -234,6 +361,12 @@ def build_groups(features: np.ndarray, w_final: np.ndarray,
     n, d, p = values.shape
     if not config.grouping:
         return GroupMap.empty(p, d)
+    if p >= KMEANS_DEVICE_MIN and _cuda_ok():
+        return build_groups_device(features, w_final, values, config,
+                                   values_dev)
+    if not isinstance(features, np.ndarray):
+        features = features.cpu().numpy()
+        w_final = w_final.cpu().numpy()
     if features.shape != (p, 2):
         raise TrainingError("feature geometry does not match frames")
     assign, _ = KMeans(config.clusters, config.cluster_seed).fit(

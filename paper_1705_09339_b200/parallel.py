@@ -379,8 +379,8 @@ class BatchEngine:
             values = torch.from_numpy(flat).to(eng.dev.device)
             _, feats, wf = train_device(proxy, values, config, bw,
                                         kde_windows, stream=s)
-            maps.append(build_groups(feats.cpu().numpy(), wf.cpu().numpy(),
-                                     flat, config, values_dev=values)
+            maps.append(build_groups(feats, wf, flat, config,
+                                     values_dev=values)
                         if config.grouping else GroupMap.empty(h * w, d))
             del values
         g = max(m.group_count for m in maps)

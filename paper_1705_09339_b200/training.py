@@ -3,7 +3,7 @@
 
 GPU: scene prior (cog_prior_build) -> GMM warm-up with mode seeding and
 grouping features (cog_gmm_warmup) -> level order (cog_set_levels).
-Host: the k-means grouping on the downloaded features (grouping.py).
+Grouping (grouping.py): on the device at scale, numpy on small frames.
 """
 
 from __future__ import annotations
@@ -93,8 +93,8 @@ def train_engine(frames, config: EngineConfig, kde_windows=None,
     eng.prior, feats, w_final = train_device(eng, values, config, bw,
                                              kde_windows)
     if config.grouping:
-        groups = build_groups(feats.cpu().numpy(), w_final.cpu().numpy(),
-                              flat, config, values_dev=values)
+        groups = build_groups(feats, w_final, flat, config,
+                              values_dev=values)
     else:
         groups = GroupMap.empty(p, d)
     install_groups(eng, groups)

@@ -96,3 +96,25 @@ def test_compare_sequences_on_a_synthetic_scene():
     js = rep.to_json()
     assert js["frames"] == 25 and "level_populations" in js
     assert "cascade F1" in rep.to_text()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("state_dtype", ["float32", "float64"])
+def test_measure_level_costs_stages_every_level(state_dtype):
+    """The level-cost calibration (evaluation.py:180-273) on the CUDA engine:
+    each of the six staged frames resolves entirely at its level (the
+    calibration raises InternalError otherwise), the costs are positive and
+    normalised by the mixture level, and the cheap levels cost no more than
+    the mixture level on the device either"""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1705_09339_b200.evaluation import (LEVEL_NAMES,
+                                                  measure_level_costs)
+    prof, secs = measure_level_costs(pixels=1 << 18, reps=5,
+                                     state_dtype=state_dtype,
+                                     return_seconds=True)
+    assert prof.gmm == 1.0
+    assert all(getattr(prof, n) > 0 for n in LEVEL_NAMES)
+    assert secs.shape == (6,) and (secs > 0).all()
+    assert prof.skipped <= 1.0 and prof.chp <= 1.0

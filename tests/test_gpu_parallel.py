@@ -267,3 +267,35 @@ def test_training_with_device_kmeans_equals_host_kmeans(name, monkeypatch):
     assert np.array_equal(a.group_id, b.group_id)
     for nm in STATE:
         assert np.array_equal(getattr(a, nm), getattr(b, nm)), nm
+
+
+@pytest.mark.parametrize("k,p", [(3, 70_001), (5, 200_000)])
+def test_device_grouping_equals_numpy(k, p, monkeypatch):
+    """build_groups_device (seeding, k-means, z-score and sigma band on the
+    device, every axis-0 reduction in numpy's row order through
+    cog_seq_sums) gives the numpy path's group map, member counts, weights
+    and pooled means bit for bit (grouping.py:100-195); duplicate points
+    exercise the lowest-index tie breaks"""
+    from paper_1705_09339_b200 import grouping
+    from paper_1705_09339_b200.config import EngineConfig
+    rng = np.random.default_rng(11 + k)
+    n, d = 12, 3
+    values = rng.integers(0, 256, (n, d, p), dtype=np.uint8)
+    feats = np.stack([rng.gamma(2, 1, p), rng.gamma(2, 1, p) * 1e-3], axis=1)
+    feats[: p // 3] *= 4.0
+    feats[p // 2: p // 2 + 500] = feats[p // 2]        # exact duplicates
+    feats[-7:] = feats[:7]
+    w_final = rng.random(p)
+    cfg = EngineConfig(color=True, clusters=k, cluster_threshold=0.9)
+    monkeypatch.setattr(grouping, "_cuda_ok", lambda: False)
+    want = grouping.build_groups(feats, w_final, values, cfg)
+    monkeypatch.undo()
+    monkeypatch.setattr(grouping, "KMEANS_DEVICE_MIN", 0)
+    got = grouping.build_groups(torch.from_numpy(feats).cuda(),
+                                torch.from_numpy(w_final).cuda(), values, cfg)
+    assert want.group_count == got.group_count > 0
+    assert np.array_equal(want.group_id, got.group_id)
+    assert np.array_equal(want.member_count, got.member_count)
+    assert np.array_equal(want.weight, got.weight)
+    assert np.array_equal(want.mu, got.mu)
+    assert np.array_equal(want.var, got.var)

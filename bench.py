@@ -6,7 +6,8 @@ K=5, trained on the first 150 frames of the seeded synthetic scene
 (paper_1705_09339_b200.synth), the largest configuration a single GPU
 holds.  A step is one frame through the step kernels.  At N>1 the 4K frame
 is split into N stride-aligned row bands, one per rank, with the frame's
-exact partials summed by one NCCL all-reduce per frame (strong scaling:
+exact partials summed over peer mailboxes inside the step's tail (or, when
+those cannot be mapped, by one NCCL all-reduce) per frame (strong scaling:
 the ranks share each frame).
 Other workloads (--workload): c3 (1920x1080, one stream per rank), c2
 (640x480, one stream per rank), c5 (64 independent 1280x720 streams split
@@ -210,15 +211,44 @@ def oracle_from_engine(eng, cfg, threads, p0=0, p1=None):
     return oe
 
 
-def cpu_baseline(frames, eng, cfg, rows, seconds, min_frames):
+def oracle_from_batch(beng, s, cfg, threads):
+    """An oracle engine holding stream s of a batch engine's state."""
+    from oracle import oracle as orc
+    oe = orc.OracleEngine(cfg, beng.height, beng.width, beng.depth)
+    oe.threads = threads
+    for k, v in beng.export_stream(s).items():
+        setattr(oe, k, np.ascontiguousarray(v))
+    dev = beng.dev
+    oe.tables = np.ascontiguousarray(dev.table[s].cpu().numpy())
+    oe.finalize_tables()
+    oe.dynamics = dev.cls[s].cpu().numpy()
+    wt = np.array([cfg.weights_static, cfg.weights_oscillating,
+                   cfg.weights_dynamic])[oe.dynamics]
+    oe.wa, oe.wb, oe.wc = (np.ascontiguousarray(wt[:, i]) for i in range(3))
+    g = dev.gid[s].cpu().numpy().astype(np.int64) & 0xFFFF
+    oe.group_id = np.where(g == 0xFFFF, -1, g)
+    G = dev.n_groups
+    gw = np.zeros(G)
+    gw[:len(beng.group_w[s])] = beng.group_w[s]
+    oe.group_w = gw
+    oe.group_members = dev.g_members[s, :G].cpu().numpy().astype(np.int64)
+    oe.frame_count = beng.frame_count
+    return oe
+
+
+def cpu_baseline(frames, eng, cfg, rows, seconds, min_frames, stream=None):
     """The oracle (1 thread: the reference's kernels are serial) seeded with
     the GPU engine's trained state, timed over a bounded sample of the same
     stream's post-training frames: at least `min_frames` frames and
     `seconds` of CPU work (cycled if the host set is shorter)."""
     os.environ["COG_ORACLE_THREADS"] = "1"
     r0, r1 = rows
-    oe = oracle_from_engine(eng, cfg, 1, r0 * eng.width, r1 * eng.width)
-    band = [np.ascontiguousarray(f[:, r0:r1]) for f in frames]
+    if stream is None:
+        oe = oracle_from_engine(eng, cfg, 1, r0 * eng.width, r1 * eng.width)
+        band = [np.ascontiguousarray(f[:, r0:r1]) for f in frames]
+    else:   # one stream of a batch engine, frames (T, S, d, H, W)
+        oe = oracle_from_batch(eng, stream, cfg, 1)
+        band = [np.ascontiguousarray(f[stream]) for f in frames]
     oe.process(band[0])  # warm
     t0 = time.perf_counter()
     done, dt = 0, 0.0
@@ -410,6 +440,67 @@ def run_reference(args):
     return 0
 
 
+def attach_band_reduce(eng, mode):
+    """How a C4 row-band rank sums the frame partials with its peers: the
+    one-shot all-reduce over peer mailboxes fused into the step's tail
+    (PeerMailbox over torch symmetric memory, else over CUDA IPC handles) --
+    adopted only if every rank could map the mailboxes AND two trial frames
+    on a clone give, on every rank, exactly the statistics the NCCL path
+    gives -- else one NCCL all-reduce per frame.  Returns the description."""
+    import torch
+    import torch.distributed as dist
+    from paper_1705_09339_b200.parallel import DistReducer, PeerMailbox
+    dev = eng.dev.device
+    nccl = "one NCCL all-reduce of the frame partials per frame"
+
+    def agreed(ok):
+        t = torch.tensor([int(ok)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
+    def trial(twin, frames):
+        stats = torch.zeros((len(frames), 16), dtype=torch.int64, device=dev)
+        mask = torch.empty((eng.height, eng.width), dtype=torch.uint8,
+                           device=dev)
+        for i, f in enumerate(frames):
+            twin.process_frame_device(f, mask, stats[i])
+        torch.cuda.synchronize(dev)
+        return stats
+
+    if mode != "nccl":
+        g = torch.Generator(device="cpu").manual_seed(1234)
+        frames = [torch.randint(0, 256, (eng.depth, eng.height, eng.width),
+                                dtype=torch.uint8, generator=g).to(dev)
+                  for _ in range(2)]
+        ref = eng.clone()
+        ref.reducer = DistReducer()
+        want = trial(ref, frames)
+        del ref
+        for name, make in (("torch symmetric memory", PeerMailbox.symmetric),
+                           ("CUDA IPC", PeerMailbox.ipc)):
+            box = None
+            try:
+                box = make(eng.depth, eng.dev.n_groups)
+            except Exception as exc:   # noqa: BLE001 - any failure = fallback
+                print(f"[bench] peer mailboxes over {name} unavailable: "
+                      f"{type(exc).__name__}: {exc}", file=sys.stderr)
+            if not agreed(box is not None):
+                continue
+            twin = eng.clone()
+            twin.peers = box
+            got = trial(twin, frames)
+            del twin
+            if agreed(bool((got == want).all())):
+                eng.peers = box
+                return (f"one-shot all-reduce of the frame partials over "
+                        f"peer mailboxes ({name}), fused into the step's "
+                        f"last CTA: no collective call, no extra launch")
+            print(f"[bench] peer mailboxes over {name}: trial frames differ "
+                  f"from the NCCL path, not used", file=sys.stderr)
+    eng.reducer = DistReducer()
+    return nccl
+
+
 class Workload:
     """One bench workload on this rank: a trained engine plus its frames.
 
@@ -466,7 +557,8 @@ class Workload:
             if world > 1:
                 self.eng = train_band_engine(train, self.cfg, rows,
                                              gather=dist_gather_rows())
-                self.eng.reducer = DistReducer()
+                self.band_reduce = attach_band_reduce(self.eng,
+                                                      args.band_reduce)
             else:
                 self.eng = train_engine(train, self.cfg)
             torch.cuda.synchronize()
@@ -548,12 +640,6 @@ class Workload:
             return (m, st), nb, self.pixels + 16 * 8
         res = eng.submit_frames(f)
         return (res,), nb, self.pixels + self.streams * 16 * 8
-        f = self.host[i % len(self.host)]
-        if self.streams == 1:
-            m, st = eng.process_frame(f)
-            return (m, st), f.nbytes, self.pixels + 16 * 8
-        res = eng.submit_frames(f)
-        return (res,), f.nbytes, self.pixels + self.streams * 16 * 8
 
     @staticmethod
     def e2e_read(res):
@@ -650,6 +736,9 @@ def main():
     ap.add_argument("--port", action="store_true",
                     help="--impl reference: time the oracle port even when "
                          "the real reference is installed (oracle/_ref)")
+    ap.add_argument("--band-reduce", default="auto", choices=["auto", "nccl"],
+                    help="c4 at N > 1: fused peer-mailbox all-reduce when it "
+                         "validates (auto), or NCCL")
     ap.add_argument("--variant", default="auto",
                     help="step kernel (engine.kernel_variant; A/B tooling)")
     ap.add_argument("--out", default="")
@@ -740,25 +829,31 @@ def main():
         cpu = None
         if not args.no_cpu and world == 1:
             r = (0, BAND_ROWS) if args.workload == "c4" else (0, spec.height)
-            eng0 = wl.eng if args.workload != "c5" else None
-            if eng0 is not None:
-                v, dt, nf = cpu_baseline(wl.host, eng0.clone(), wl.cfg, r,
+            if args.workload == "c5":
+                v, dt, nf = cpu_baseline(wl.host, wl.eng, wl.cfg, r,
+                                         args.cpu_seconds, args.cpu_frames,
+                                         stream=0)
+                what = "stream 0 (of the last wave) of the"
+            else:
+                v, dt, nf = cpu_baseline(wl.host, wl.eng.clone(), wl.cfg, r,
                                          args.cpu_seconds, args.cpu_frames)
-                what = (f"rows {r[0]}-{r[1] - 1} of" if args.workload == "c4"
-                        else "the whole")
-                cpu = {"value": v, "unit": "pixel-frames/s", "cores": 1,
-                       "kind": "port",
-                       "sample": f"{nf} post-training frames of {what} "
-                                 f"{args.workload.upper()} frame, from the "
-                                 f"GPU engine's trained state; oracle C "
-                                 f"kernels (restatement of the serial numba "
-                                 f"kernels), 1 thread, {dt:.1f}s"}
+                what = (f"rows {r[0]}-{r[1] - 1} of the"
+                        if args.workload == "c4" else "the whole")
+            cpu = {"value": v, "unit": "pixel-frames/s", "cores": 1,
+                   "kind": "port",
+                   "sample": f"{nf} post-training frames of {what} "
+                             f"{args.workload.upper()} frame, from the "
+                             f"GPU engine's state; oracle C "
+                             f"kernels (restatement of the serial numba "
+                             f"kernels), 1 thread, {dt:.1f}s"}
         traffic = None
         tpath = ROOT / "profiles" / f"traffic_{args.workload}.json"
         if tpath.exists():
             traffic = json.loads(tpath.read_text()).get("bytes_per_step")
-        frac_bytes = min(b_step, traffic) if traffic else b_step
-        achieved = frac_bytes / (step_ms * 1e-3) / 1e9
+        # the contract's definition: algorithmic bytes (SURVEY 8(d) model
+        # over this run's own level populations) / measured duration; the
+        # ncu DRAM traffic of the same step is reported beside it
+        achieved = b_step / (step_ms * 1e-3) / 1e9
         lvl = rows[:, 1:7].sum(axis=0) / max(1, rows[:, 1:7].sum())
         wave_txt = (f", {len(waves)} wave(s) of <= {args.streams} resident "
                     f"streams per rank" if args.workload == "c5" else "")
@@ -782,9 +877,9 @@ def main():
                        "l2": "flushed between steps (256 MiB write, "
                              "untimed); the per-frame state is also far "
                              "larger than L2",
-                       "parallelism": (f"{world} row band(s), one NCCL "
-                                       f"all-reduce of the frame partials "
-                                       f"per frame" if args.workload == "c4"
+                       "parallelism": (f"{world} row band(s), "
+                                       f"{wl.band_reduce}"
+                                       if args.workload == "c4"
                                        and world > 1 else
                                        f"{world} rank(s), independent "
                                        f"streams{wave_txt}")},
@@ -797,8 +892,9 @@ def main():
                          "frac": achieved / peak,
                          "algorithmic_bytes_per_step": b_step,
                          "traffic": traffic,
-                         "bytes_used": "min(algorithmic, traffic)"
-                                       if traffic else "algorithmic"},
+                         "bytes_used": "algorithmic (SURVEY 8(d) model); "
+                                       "traffic = ncu DRAM bytes of the "
+                                       "same step"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "pixel-frames/s",
                     "h2d_bytes_per_step": int(bi // len(waves)),

@@ -196,6 +196,40 @@ int cog_finalize(const cog_geom *geom, const cog_params *prm,
                  const cog_state *st, int64_t *stats, int64_t frame_index,
                  void *stream);
 
+/* Row-band shards on several GPUs: the cross-shard sum of the frame's exact
+ * partials (what cascade.py:301-313, 320-344 computes over the whole frame)
+ * as a one-shot all-reduce over peer memory, fused into the step's tail.
+ * Every rank owns a mailbox of cog_mailbox_words() u64 words, mapped into
+ * every peer (CUDA IPC / symmetric memory): [2 parities][n_ranks slots]
+ * [accum words + 1 flag].  The last CTA of the step stores the rank's
+ * partials into its slot of EVERY rank's mailbox (stores over NVLink), then
+ * the flag (= seq, release at system scope); it -- fuse = 1 -- or
+ * cog_finalize_p2p -- fuse = 0 -- waits for the n_ranks flags of its own
+ * mailbox (acquire), sums the slots (integers: any order gives the same
+ * sum) and runs the frame tail, identically on every rank.  seq > 0 must
+ * be the same on every rank for the same frame and grow by one per step;
+ * slots alternate by seq parity (a rank can only be one step ahead).
+ * fuse = 1 makes the kernels of different ranks wait on one another: one
+ * shard per GPU only.  streams must be 1. */
+#define COG_MAX_RANKS 16
+typedef struct cog_peers {
+  int32_t n_ranks, rank;
+  uint64_t seq;
+  uint64_t *mailbox[COG_MAX_RANKS]; /* rank r's mailbox, as mapped here */
+} cog_peers;
+
+int64_t cog_mailbox_words(int32_t depth, int32_t n_groups, int32_t n_ranks);
+
+int cog_step_p2p(const cog_geom *geom, const cog_params *prm,
+                 const cog_state *st, const uint8_t *frame, uint8_t *mask,
+                 void *conf, uint8_t *kind, int64_t *stats,
+                 int64_t frame_index, int32_t reorder_now, int32_t fuse,
+                 const cog_peers *peers, void *stream);
+
+int cog_finalize_p2p(const cog_geom *geom, const cog_params *prm,
+                     const cog_state *st, int64_t *stats, int64_t frame_index,
+                     const cog_peers *peers, void *stream);
+
 /* Materialise a pending illumination reset (device flag) and/or a level
  * reorder (reorder_now) so the state reads as the reference's would. */
 int cog_apply_pending(const cog_geom *geom, const cog_params *prm,

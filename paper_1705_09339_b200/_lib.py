@@ -106,6 +106,16 @@ class State(ctypes.Structure):
         "deepq", "deeprho", "hitq")]
 
 
+MAX_RANKS = 16
+
+
+class Peers(ctypes.Structure):
+    """cog_peers: the peer mailboxes of a row-band shard (cog_step_p2p)."""
+    _fields_ = [("n_ranks", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("seq", ctypes.c_uint64),
+                ("mailbox", ctypes.c_void_p * MAX_RANKS)]
+
+
 class RefState(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "mu", "var", "w", "count", "mid", "ref", "chp", "label", "active",
@@ -130,6 +140,13 @@ _SIGS = {
                                 ctypes.c_int64, ctypes.c_int32,
                                 ctypes.c_int32, _P]),
     "cog_finalize": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int64, _P]),
+    "cog_mailbox_words": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.c_int32]),
+    "cog_step_p2p": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P,
+                                    ctypes.c_int64, ctypes.c_int32,
+                                    ctypes.c_int32, _P, _P]),
+    "cog_finalize_p2p": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int64, _P,
+                                        _P]),
     "cog_apply_pending": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, _P]),
     "cog_baseline_frame": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "cog_export_state": (ctypes.c_int, [_P, _P, _P, _P]),

@@ -478,6 +478,9 @@ class CascadeEngine:
         # row-band shard: callable summing the `accum` partials across the
         # shards of one frame in place (parallel.py); None = whole frame
         self.reducer = None
+        # row-band shard on its own GPU: parallel.PeerMailbox -- the sum of
+        # the partials fused into the step over peer memory (no reducer)
+        self.peers = None
         self._ring = None  # pinned host staging, created on first host frame
 
     # ------------------------------------------------------------ helpers
@@ -609,6 +612,28 @@ class CascadeEngine:
         banded = self.reducer is not None
         geom, prm, st = (_lib.ref(self.dev.geom), _lib.ref(self._params()),
                          _lib.ref(self.dev.cstate))
+        if self.peers is not None:
+            # row-band shard on its own GPU: the cross-shard sum is fused
+            # into the step's tail over peer mailboxes (parallel.PeerMailbox)
+            box = self.peers
+            if not box.fused and box.barrier is None:
+                raise DataError("a local (one-process) peer mailbox is "
+                                "stepped by BandSet, not by its engines")
+            rc = self.lib.cog_step_p2p(
+                geom, prm, st, x.data_ptr(), mask.data_ptr(),
+                self.dev.conf.data_ptr(), self.dev.kind.data_ptr(),
+                stats.data_ptr(), self.frame_count,
+                int(self._reorder_pending), int(box.fused),
+                _lib.ref(box.next()), self.stream)
+            _lib.check(rc, "cog_step_p2p")
+            if not box.fused:
+                box.barrier()   # every rank's push has landed
+                rc = self.lib.cog_finalize_p2p(
+                    geom, prm, st, stats.data_ptr(), self.frame_count,
+                    _lib.ref(box.current()), self.stream)
+                _lib.check(rc, "cog_finalize_p2p")
+            self._advance()
+            return
         rc = self.lib.cog_step(
             geom, prm, st, x.data_ptr(), mask.data_ptr(),
             self.dev.conf.data_ptr(), self.dev.kind.data_ptr(),
@@ -654,7 +679,7 @@ class CascadeEngine:
                 self._stage(frame, slot["in"].numpy())
                 src = slot["in"]
             slot["src"] = src
-        if not cuda_in and self.reducer is None:
+        if not cuda_in and self.reducer is None and self.peers is None:
             rc = self.lib.cog_step_host(
                 _lib.ref(self.dev.geom), _lib.ref(self._params()),
                 _lib.ref(self.dev.cstate), src.data_ptr(),

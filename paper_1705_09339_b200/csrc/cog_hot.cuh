@@ -154,6 +154,54 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// A warp's buffered worklist items go out two-ended, so that the deep pass
+// runs warps of one item type: fp32 MEANVAR updates grow from the front of
+// the stream's worklist (count in sync[2]), GMM fall-throughs and deferred
+// plane-pixels from its back (count in sync[3]); one 64-bit atomic reserves
+// both ranges.  The capacity is every plane-pixel, so the ends cannot meet.
+static_assert(HQ_CAP == 64, "hot_flush moves two entries per lane");
+__device__ __forceinline__ void hot_flush(const unsigned long long* qc,
+                                          const double* qr, int n,
+                                          uint32_t* sync,
+                                          unsigned long long* dq_code,
+                                          double* dq_rho, size_t dq_cap,
+                                          int lane) {
+  __syncwarp();
+  const bool v0 = lane < n, v1 = lane + 32 < n;
+  const unsigned long long c0 = v0 ? qc[lane] : 0ull;
+  const unsigned long long c1 = v1 ? qc[lane + 32] : 0ull;
+  const bool a0 = v0 && ((c0 >> 1) & 3ull) == (unsigned long long)DEEP_MEANVAR &&
+                  !(c0 & ITEM_DEFERRED);
+  const bool a1 = v1 && ((c1 >> 1) & 3ull) == (unsigned long long)DEEP_MEANVAR &&
+                  !(c1 & ITEM_DEFERRED);
+  const unsigned ma0 = __ballot_sync(FULL, a0), ma1 = __ballot_sync(FULL, a1);
+  const unsigned mb0 = __ballot_sync(FULL, v0 && !a0);
+  const unsigned mb1 = __ballot_sync(FULL, v1 && !a1);
+  const unsigned na = __popc(ma0) + __popc(ma1);
+  unsigned long long old = 0ull;
+  if (lane == 0)
+    old = atomicAdd(reinterpret_cast<unsigned long long*>(sync + 2),
+                    (unsigned long long)na |
+                        ((unsigned long long)((unsigned)n - na) << 32));
+  const unsigned base_a = __shfl_sync(FULL, (unsigned)old, 0);
+  const unsigned base_b = __shfl_sync(FULL, (unsigned)(old >> 32), 0);
+  const unsigned lt = (1u << lane) - 1u;
+  if (v0) {
+    const size_t i = a0 ? (size_t)base_a + __popc(ma0 & lt)
+                        : dq_cap - 1 - ((size_t)base_b + __popc(mb0 & lt));
+    dq_code[i] = c0;
+    dq_rho[i] = qr[lane];
+  }
+  if (v1) {
+    const size_t i =
+        a1 ? (size_t)base_a + __popc(ma0) + __popc(ma1 & lt)
+           : dq_cap - 1 - ((size_t)base_b + __popc(mb0) + __popc(mb1 & lt));
+    dq_code[i] = c1;
+    dq_rho[i] = qr[lane + 32];
+  }
+  __syncwarp();
+}
+
 // compile-time configuration of a hot_kernel instantiation: FL < 0 reads
 // the feature switches from the params, else bit 0 sampling, 1 grouping,
 // 2 change-hypothesis probe, 3 rate scaling, 4 literal confidence; ST = 0
@@ -366,8 +414,16 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
     uint32_t q16 = 0u;
     in.m0 = make_float2(0.0f, 1.0f);
     in.m1 = in.m0;
+#if defined(HOT_EXP_LINEAR)   // cost attribution only (tools/gpu_ab_build.sh): wrong results
+    if (ev) q16 = __ldcg(tq + ((size_t)t * 256 + 128) * 32);
+#else
     if (ev) q16 = __ldcg(tq + ((size_t)t * 256 + vb) * 32);
+#endif
+#if defined(HOT_EXP_NOMODES)
+    if (false) {
+#else
     if (need) {
+#endif
       in.m0 = *reinterpret_cast<const float2*>(rec + 2 * r0);
       in.m1 = *reinterpret_cast<const float2*>(rec + 2 * r1);
     }
@@ -640,8 +696,13 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
       if (fast) {
         a.s.streak[o] = skn;
         // one dense RED per plane-pixel: a byte per level below GMM
+#if defined(HOT_EXP_NORED)
+        if (hitq != nullptr && active < L_GMM)
+          ;
+#else
         if (hitq != nullptr && active < L_GMM)
           atomicAdd(hitq + o, 1u << (8 * active));
+#endif
         else
           atomicAdd(a.s.hits + (plane * 5 + (uint32_t)active * P + p), 1u);
         if (active == L_MEAN)
@@ -667,15 +728,7 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
     if (qm) {
       const int nq = __popc(qm);
       if (wq_n + nq > HQ_CAP) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(sync + 3, (unsigned)wq_n);
-        base = __shfl_sync(FULL, base, 0);
-        __syncwarp();
-        for (int e = lane; e < wq_n; e += 32) {
-          dq_code[(size_t)base + e] = qc[e];
-          dq_rho[(size_t)base + e] = qr[e];
-        }
-        __syncwarp();
+        hot_flush(qc, qr, wq_n, sync, dq_code, dq_rho, dq_cap, lane);
         wq_n = 0;
       }
       if (item) {
@@ -705,8 +758,10 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
 
     // ---- outputs, kind counts
     if (valid && !deferred) {
+#if !defined(HOT_EXP_NOCONF)
       conf_s[o] = cf;
       a.kind[o] = (uint8_t)kind;
+#endif
       kc += 1ull << (9 * kind);
     }
 
@@ -798,16 +853,7 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
       }
     }
   }
-  if (wq_n) {
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(sync + 3, (unsigned)wq_n);
-    base = __shfl_sync(FULL, base, 0);
-    __syncwarp();
-    for (int e = lane; e < wq_n; e += 32) {
-      dq_code[(size_t)base + e] = qc[e];
-      dq_rho[(size_t)base + e] = qr[e];
-    }
-  }
+  if (wq_n) hot_flush(qc, qr, wq_n, sync, dq_code, dq_rho, dq_cap, lane);
 #pragma unroll
   for (int q = 0; q < 7; ++q) {
     const unsigned v = warp_sum_u32((unsigned)((kc >> (9 * q)) & 511u));

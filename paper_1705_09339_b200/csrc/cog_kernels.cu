@@ -84,6 +84,8 @@ struct StepArgs {
   int reorder_now;
   int fuse_finalize;
   int cw, iters, tiles_x, n_tiles;
+  int two_ended;  // the worklist was filled from both ends (hot_flush)
+  cog_peers peers;  // n_ranks > 1: cross-shard sum over peer mailboxes
 };
 
 // ---------------------------------------------------------------------------
@@ -686,6 +688,87 @@ __device__ double exact_group_conf(const StepArgs& a, int s, int c, int g) {
   for (size_t p = 0; p < P; ++p)
     if (kind[p] == L_GROUP && gid[p] == (uint16_t)g) acc = acc + (double)conf[p];
   return acc;
+}
+
+// ---------------------------------------------------------------------------
+// One-shot all-reduce of a row-band shard's frame partials over peer
+// mailboxes (include/cog_b200.h, cog_peers).  Both run in ONE CTA, after
+// every CTA's contribution has reached `acc` (the caller's done counter).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys(unsigned long long* p,
+                                               unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(
+    const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(
+    const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// this rank's partials into its slot of every rank's mailbox, then the flags
+__device__ void p2p_push(const cog_peers& pr, const unsigned long long* acc,
+                         int words) {
+  const size_t slot = (size_t)words + 1;
+  const size_t off =
+      ((size_t)(pr.seq & 1ull) * (size_t)pr.n_ranks + (size_t)pr.rank) * slot;
+  for (int r = 0; r < pr.n_ranks; ++r) {
+    unsigned long long* dst = (unsigned long long*)pr.mailbox[r] + off;
+    for (int i = threadIdx.x; i < words; i += blockDim.x)
+      dst[i] = __ldcg(acc + i);
+  }
+  __threadfence_system();
+  __syncthreads();
+  if ((int)threadIdx.x < pr.n_ranks)
+    st_release_sys((unsigned long long*)pr.mailbox[threadIdx.x] + off + words,
+                   pr.seq);
+}
+
+// wait for every rank's slot of this step in the own mailbox; acc = their
+// sum.  The wait is bounded (P2P_WAIT_NS): a peer that never arrives must
+// not hang the GPU -- returns false then (the frame's sums are incomplete;
+// the caller flags the frame's stats row)
+constexpr unsigned long long P2P_WAIT_NS = 10ull * 1000 * 1000 * 1000;
+__device__ bool p2p_wait_sum(const cog_peers& pr, unsigned long long* acc,
+                             int words) {
+  __shared__ int s_late;
+  const size_t slot = (size_t)words + 1;
+  const unsigned long long* box = (const unsigned long long*)pr.mailbox[pr.rank] +
+                                  (size_t)(pr.seq & 1ull) * (size_t)pr.n_ranks * slot;
+  if (threadIdx.x == 0) s_late = 0;
+  __syncthreads();
+  if ((int)threadIdx.x < pr.n_ranks) {
+    const unsigned long long* flag = box + (size_t)threadIdx.x * slot + words;
+    unsigned long long t0 = 0, spins = 0;
+    while (ld_acquire_sys(flag) != pr.seq) {
+      __nanosleep(64);
+      if ((++spins & 1023ull) == 0) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > P2P_WAIT_NS) {
+          s_late = 1;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < words; i += blockDim.x) {
+    unsigned long long v = 0ull;
+    for (int r = 0; r < pr.n_ranks; ++r)
+      v += ld_relaxed_sys(box + (size_t)r * slot + i);
+    acc[i] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  return s_late == 0;
 }
 
 template <typename T>
@@ -1743,7 +1826,14 @@ __global__ void __launch_bounds__(DEEP_THREADS, DEEP_MINB) deep_kernel(const Ste
   const size_t dq_cap = dq_capacity(d, P);
   unsigned long long* dq_code = (unsigned long long*)a.s.deepq + (size_t)s * dq_cap;
   const double* dq_rho = a.s.deeprho + (size_t)s * dq_cap;
-  const size_t n = *(volatile uint32_t*)(sync + 3);
+  // hot_kernel's worklist is two-ended (cog_hot.cuh, hot_flush): n_a items
+  // at the front, n_b at the back; virtual index i runs over the front
+  // items, a gap up to the next warp boundary, then the back items -- so a
+  // warp holds one item type.  Every other step kernel fills the front only
+  const size_t n_b = *(volatile uint32_t*)(sync + 3);
+  const size_t n_a = a.two_ended ? *(volatile uint32_t*)(sync + 2) : n_b;
+  const size_t a32 = (n_a + 31) & ~(size_t)31;
+  const size_t n = a.two_ended ? a32 + n_b : n_a;
   if (threadIdx.x == 0) s_fg = 0;
   __syncthreads();
   unsigned fg = 0;
@@ -1755,8 +1845,10 @@ __global__ void __launch_bounds__(DEEP_THREADS, DEEP_MINB) deep_kernel(const Ste
   // few CTAs
   const size_t wpc = blockDim.x >> 5;
   const size_t gw = (size_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-  for (size_t i = gw * 32 + (threadIdx.x & 31); i < n;
-       i += (size_t)gridDim.x * wpc * 32) {
+  for (size_t vi = gw * 32 + (threadIdx.x & 31); vi < n;
+       vi += (size_t)gridDim.x * wpc * 32) {
+    if (vi >= n_a && vi < a32) continue;
+    const size_t i = vi < n_a ? vi : dq_cap - 1 - (vi - a32);
     const unsigned long long code = dq_code[i];
     if (!(code & 1ull)) continue;
     dq_code[i] = 0ull;
@@ -1782,7 +1874,8 @@ __global__ void __launch_bounds__(DEEP_THREADS, DEEP_MINB) deep_kernel(const Ste
   if ((threadIdx.x & 31) == 0 && fg) atomicAdd(&s_fg, (unsigned long long)fg);
   __syncthreads();
   if (threadIdx.x == 0 && s_fg) atomicAdd(gacc + acc_fg(d), s_fg);
-  if (!a.fuse_finalize) return;
+  const bool p2p = a.peers.n_ranks > 1;
+  if (!a.fuse_finalize && !p2p) return;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1792,6 +1885,17 @@ __global__ void __launch_bounds__(DEEP_THREADS, DEEP_MINB) deep_kernel(const Ste
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  if (p2p) {
+    // row-band shard: the partials go to every rank's mailbox from here;
+    // fused, this CTA also waits for the other shards' and sums them
+    p2p_push(a.peers, gacc, words);
+    if (!a.fuse_finalize) return;
+    const bool in_time = p2p_wait_sum(a.peers, gacc, words);
+    finalize_stream<T>(a, s, gacc, a.stats, sync);
+    if (!in_time && threadIdx.x == 0)
+      a.stats[(size_t)s * STATS_WORDS + STATS_WORDS - 1] = -1;  // peer missing
+    return;
+  }
   finalize_stream<T>(a, s, gacc, a.stats, sync);
 }
 
@@ -1818,8 +1922,12 @@ template <typename T>
 __global__ void finalize_kernel(const StepArgs a) {
   const int s = blockIdx.x;
   const int words = acc_words(a.g.depth, a.g.n_groups);
-  finalize_stream<T>(a, s, (unsigned long long*)a.s.accum + (size_t)s * words,
-                     a.stats, a.s.sync + (size_t)s * 4);
+  unsigned long long* acc = (unsigned long long*)a.s.accum + (size_t)s * words;
+  bool in_time = true;
+  if (a.peers.n_ranks > 1) in_time = p2p_wait_sum(a.peers, acc, words);
+  finalize_stream<T>(a, s, acc, a.stats, a.s.sync + (size_t)s * 4);
+  if (!in_time && threadIdx.x == 0)
+    a.stats[(size_t)s * STATS_WORDS + STATS_WORDS - 1] = -1;  // peer missing
 }
 
 template <typename T, int KMAX>
@@ -2790,13 +2898,15 @@ int launch_step(const StepArgs& a, cudaStream_t st) {
   ensure_bterm();
   // float32 state: the fast kernel; otherwise lean / general
   const bool fast = fast_ok(a, sizeof(T) == 4);
-  int rc = fast ? (a.q.variant == 3 ? launch_fast(a, st) : launch_hotpass(a, st))
-                : launch_hot<T>(a, st);
+  StepArgs b = a;
+  b.two_ended = fast && a.q.variant != 3;
+  int rc = fast ? (a.q.variant == 3 ? launch_fast(b, st) : launch_hotpass(b, st))
+                : launch_hot<T>(b, st);
   if (rc) return rc;
   // programmatic dependent launch of the deep pass behind the fast kernel:
   // its CTAs are scheduled while the hot kernel drains (they wait in
   // griddepcontrol.wait), which hides the launch gap
-  return launch_deep<T>(a, st, fast);
+  return launch_deep<T>(b, st, fast);
 }
 
 }  // namespace
@@ -3080,6 +3190,66 @@ int cog_finalize(const cog_geom* geom, const cog_params* prm,
     finalize_kernel<double><<<geom->streams, 128, 0, (cudaStream_t)stream>>>(a);
   else
     finalize_kernel<float><<<geom->streams, 128, 0, (cudaStream_t)stream>>>(a);
+  return launch_status();
+}
+
+int64_t cog_mailbox_words(int32_t depth, int32_t n_groups, int32_t n_ranks) {
+  if (depth < 1 || depth > MAXD || n_groups < 0 || n_ranks < 1 ||
+      n_ranks > COG_MAX_RANKS)
+    return -1;
+  return 2ll * n_ranks * ((int64_t)acc_words(depth, n_groups) + 1);
+}
+
+static int check_peers(const cog_geom* geom, const cog_peers* pr) {
+  if (!pr || pr->n_ranks < 2 || pr->n_ranks > COG_MAX_RANKS || pr->rank < 0 ||
+      pr->rank >= pr->n_ranks || pr->seq == 0 || geom->streams != 1)
+    return COG_EINVAL;
+  for (int r = 0; r < pr->n_ranks; ++r)
+    if (!pr->mailbox[r]) return COG_EINVAL;
+  return COG_OK;
+}
+
+int cog_step_p2p(const cog_geom* geom, const cog_params* prm,
+                 const cog_state* st, const uint8_t* frame, uint8_t* mask,
+                 void* conf, uint8_t* kind, int64_t* stats,
+                 int64_t frame_index, int32_t reorder_now, int32_t fuse,
+                 const cog_peers* peers, void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!prm || !st || !frame || !mask || !conf || !kind || !stats)
+    return COG_EINVAL;
+  rc = check_peers(geom, peers);
+  if (rc) return rc;
+  StepArgs a = make_args(geom, prm, st);
+  a.frame = frame;
+  a.mask = mask;
+  a.conf = conf;
+  a.kind = kind;
+  a.stats = stats;
+  a.frame_index = frame_index;
+  a.reorder_now = reorder_now;
+  a.fuse_finalize = fuse ? 1 : 0;
+  a.peers = *peers;
+  cudaStream_t s = (cudaStream_t)stream;
+  return geom->state_f64 ? launch_step<double>(a, s) : launch_step<float>(a, s);
+}
+
+int cog_finalize_p2p(const cog_geom* geom, const cog_params* prm,
+                     const cog_state* st, int64_t* stats, int64_t frame_index,
+                     const cog_peers* peers, void* stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!prm || !st || !stats) return COG_EINVAL;
+  rc = check_peers(geom, peers);
+  if (rc) return rc;
+  StepArgs a = make_args(geom, prm, st);
+  a.stats = stats;
+  a.frame_index = frame_index;
+  a.peers = *peers;
+  if (geom->state_f64)
+    finalize_kernel<double><<<1, 128, 0, (cudaStream_t)stream>>>(a);
+  else
+    finalize_kernel<float><<<1, 128, 0, (cudaStream_t)stream>>>(a);
   return launch_status();
 }
 

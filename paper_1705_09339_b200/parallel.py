@@ -102,6 +102,130 @@ class DistReducer:
         dist.all_reduce(accum, op=dist.ReduceOp.SUM, group=self.group)
 
 
+class PeerMailbox:
+    """One row-band shard's side of the fused cross-shard sum
+    (``cog_step_p2p``, include/cog_b200.h ``cog_peers``): every rank's
+    mailbox mapped into this process, this rank's index and the step
+    sequence number.  With it set as ``engine.peers`` a frame is two kernels
+    on every rank -- hot pass, deep pass -- and the deep pass's last CTA
+    stores the frame's partials into every peer's mailbox over NVLink, waits
+    for theirs and runs the frame tail: no NCCL call, no host
+    synchronisation, no extra launch per frame.
+
+    The sequence number is shared by every engine holding this object (an
+    engine and its clones), so ranks that issue the same sequence of steps
+    -- SPMD -- stay in step."""
+
+    def __init__(self, depth: int, n_groups: int, n_ranks: int, rank: int,
+                 ptrs: Sequence[int], keep=None, fused: bool = True,
+                 barrier: Callable[[], None] | None = None):
+        if not 2 <= n_ranks <= _lib.MAX_RANKS or len(ptrs) != n_ranks:
+            raise DataError(f"peer mailbox over {n_ranks} ranks")
+        self.n_ranks, self.rank = n_ranks, rank
+        self.ptrs = [int(x) for x in ptrs]
+        self.keep = keep          # the allocations behind the pointers
+        self.fused = fused
+        # unfused across processes (ranks sharing a GPU): called between a
+        # step's push and its cog_finalize_p2p, after which every rank's
+        # push has landed -- so no kernel waits for one that cannot run
+        self.barrier = barrier
+        self.seq = 0
+        self.words = int(_lib.load().cog_mailbox_words(depth, n_groups,
+                                                       n_ranks))
+        self._c = _lib.Peers()
+        self._c.n_ranks, self._c.rank = n_ranks, rank
+        for r, ptr in enumerate(self.ptrs):
+            self._c.mailbox[r] = ptr
+
+    def next(self) -> "_lib.Peers":
+        """The peers struct of the next step."""
+        self.seq += 1
+        self._c.seq = self.seq
+        return self._c
+
+    def current(self) -> "_lib.Peers":
+        return self._c
+
+    @staticmethod
+    def size(depth: int, n_groups: int, n_ranks: int) -> int:
+        n = int(_lib.load().cog_mailbox_words(depth, n_groups, n_ranks))
+        if n < 0:
+            raise DataError(f"peer mailbox over {n_ranks} ranks")
+        return n
+
+    @classmethod
+    def local(cls, depth: int, n_groups: int, n_ranks: int,
+              device=None) -> list["PeerMailbox"]:
+        """All ranks' mailboxes in one process on one GPU (``BandSet``, the
+        single-GPU parity tests): the unfused form -- every band's step
+        pushes, then every band's ``cog_finalize_p2p`` finds its flags set
+        -- so no kernel ever waits on a later one."""
+        n = cls.size(depth, n_groups, n_ranks)
+        boxes = [torch.zeros(n, dtype=torch.int64, device=device or "cuda")
+                 for _ in range(n_ranks)]
+        ptrs = [b.data_ptr() for b in boxes]
+        return [cls(depth, n_groups, n_ranks, r, ptrs, keep=boxes,
+                    fused=False) for r in range(n_ranks)]
+
+    @classmethod
+    def symmetric(cls, depth: int, n_groups: int,
+                  group=None) -> "PeerMailbox":
+        """One rank per GPU: the mailboxes are torch symmetric memory
+        (peer-mapped over NVLink), exchanged through the process group."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        group = group if group is not None else dist.group.WORLD
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        n = cls.size(depth, n_groups, world)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        box = symm.empty(n, dtype=torch.int64, device=dev)
+        box.zero_()
+        hdl = symm.rendezvous(box, group)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group)     # every mailbox is zero before any push
+        return cls(depth, n_groups, world, rank, list(hdl.buffer_ptrs),
+                   keep=(box, hdl), fused=True)
+
+
+    @classmethod
+    def ipc(cls, depth: int, n_groups: int, group=None,
+            fused: bool = True) -> "PeerMailbox":
+        """The mailboxes as plain device allocations shared through CUDA IPC
+        handles (torch's storage sharing), exchanged over the process group.
+        ``fused=False`` is for ranks that share one GPU (the two-process
+        test): push, host barrier, then ``cog_finalize_p2p``."""
+        import torch.distributed as dist
+        group = group if group is not None else dist.group.WORLD
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        n = cls.size(depth, n_groups, world)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        box = torch.zeros(n, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize(dev)
+        handles = [None] * world
+        dist.all_gather_object(handles, box.untyped_storage()._share_cuda_(),
+                               group=group)
+        keep, ptrs = [box], []
+        for r, h in enumerate(handles):
+            if r == rank:
+                ptrs.append(box.data_ptr())
+                continue
+            with torch.cuda.device(h[0]):
+                st = torch.UntypedStorage._new_shared_cuda(*h)
+            peer = torch.empty(0, dtype=torch.int64,
+                               device=st.device).set_(st)
+            if peer.device != dev:
+                peer[:1].to(dev)    # enables peer access dev -> owner
+            keep.append(peer)
+            ptrs.append(peer.data_ptr())
+        dist.barrier(group)
+
+        def barrier():
+            torch.cuda.current_stream(dev).synchronize()
+            dist.barrier(group)
+        return cls(depth, n_groups, world, rank, ptrs, keep=keep, fused=fused,
+                   barrier=None if fused else barrier)
+
+
 def dist_gather_rows(group=None) -> Gather:
     """Gather callable for ``train_band_engine``: all-gathers the per-band
     feature rows of every rank (in rank = band order)."""
@@ -194,6 +318,9 @@ class BandSet:
         self.engines = list(engines)
         if not self.engines:
             raise DataError("BandSet needs at least one band")
+        # set by use_mailboxes(): the bands sum their partials through peer
+        # mailboxes (the multi-GPU data path, unfused) instead of torch ops
+        self.mailboxes = None
         e0 = self.engines[0]
         self.width, self.depth = e0.width, e0.depth
         self.height = sum(e.height for e in self.engines)
@@ -237,9 +364,43 @@ class BandSet:
             _lib.check(rc, "cog_set_levels")
         return cls(engines)
 
+    def use_mailboxes(self) -> None:
+        """Sum the bands' partials the way ranks on several GPUs do
+        (``PeerMailbox``): each band's step pushes into every band's
+        mailbox, each band's ``cog_finalize_p2p`` sums its own."""
+        if len(self.engines) < 2:
+            raise DataError("mailboxes need at least two bands")
+        e0 = self.engines[0]
+        self.mailboxes = PeerMailbox.local(e0.depth, e0.dev.n_groups,
+                                           len(self.engines), e0.dev.device)
+
+    def _frame_p2p(self, frame, mask, stats) -> None:
+        bands = []
+        for eng, box, (r0, r1) in zip(self.engines, self.mailboxes, self.rows):
+            eng._flush()
+            st = torch.empty(16, dtype=torch.int64, device=stats.device)
+            x = frame[:, r0:r1].contiguous()
+            geom, prm, cst = (_lib.ref(eng.dev.geom), _lib.ref(eng._params()),
+                              _lib.ref(eng.dev.cstate))
+            rc = eng.lib.cog_step_p2p(
+                geom, prm, cst, x.data_ptr(), mask[r0:r1].data_ptr(),
+                eng.dev.conf.data_ptr(), eng.dev.kind.data_ptr(),
+                st.data_ptr(), eng.frame_count, int(eng._reorder_pending), 0,
+                _lib.ref(box.next()), eng.stream)
+            _lib.check(rc, "cog_step_p2p")
+            bands.append((eng, box, geom, prm, cst, x))
+        for eng, box, geom, prm, cst, x in bands:
+            rc = eng.lib.cog_finalize_p2p(geom, prm, cst, stats.data_ptr(),
+                                          eng.frame_count,
+                                          _lib.ref(box.current()), eng.stream)
+            _lib.check(rc, "cog_finalize_p2p")
+            eng._advance()
+
     def process_frame_device(self, frame: torch.Tensor, mask: torch.Tensor,
                              stats: torch.Tensor) -> None:
         """frame (d, H, W) u8, mask (H, W) u8, stats (16,) i64 -- CUDA."""
+        if self.mailboxes is not None:
+            return self._frame_p2p(frame, mask, stats)
         bands = []
         for eng, (r0, r1) in zip(self.engines, self.rows):
             eng._flush()

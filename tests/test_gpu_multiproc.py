@@ -39,10 +39,10 @@ def _cfg(dtype):
                         reorder_interval=10).validate()
 
 
-def _rank(rank, world, port, dtype, out_dir):
+def _rank(rank, world, port, dtype, out_dir, mailbox=False):
     import torch.distributed as dist
-    from paper_1705_09339_b200.parallel import (DistReducer, band_rows,
-                                                dist_gather_rows,
+    from paper_1705_09339_b200.parallel import (DistReducer, PeerMailbox,
+                                                band_rows, dist_gather_rows,
                                                 train_band_engine)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -53,7 +53,12 @@ def _rank(rank, world, port, dtype, out_dir):
     rows = band_rows(frames.shape[2], world, cfg.stride)[rank]
     eng = train_band_engine(frames[:N_TRAIN], cfg, rows,
                             gather=dist_gather_rows())
-    eng.reducer = DistReducer()
+    if mailbox:
+        # the ranks share cuda:0, so the unfused form: push over CUDA IPC
+        # peer memory, host barrier, cog_finalize_p2p
+        eng.peers = PeerMailbox.ipc(eng.depth, eng.dev.n_groups, fused=False)
+    else:
+        eng.reducer = DistReducer()
     masks, stats = [], []
     for t in range(N_TRAIN, N_TRAIN + N_RUN):
         m, st = eng.process_frame(np.ascontiguousarray(frames[t][:, rows[0]:rows[1]]))
@@ -71,8 +76,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("mailbox", [False, True])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
-def test_two_process_row_bands_equal_single_engine(dtype):
+def test_two_process_row_bands_equal_single_engine(dtype, mailbox):
+    """mailbox=True: the partials cross the process boundary through peer
+    mailboxes mapped with CUDA IPC (cog_step_p2p pushes from the step's last
+    CTA, cog_finalize_p2p sums) instead of the host all-reduce"""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_1705_09339_b200.training import train_engine
@@ -80,7 +89,8 @@ def test_two_process_row_bands_equal_single_engine(dtype):
     with tempfile.TemporaryDirectory() as tmp:
         ctx = mp.get_context("spawn")
         port = _free_port()
-        procs = [ctx.Process(target=_rank, args=(r, world, port, dtype, tmp))
+        procs = [ctx.Process(target=_rank,
+                             args=(r, world, port, dtype, tmp, mailbox))
                  for r in range(world)]
         for p in procs:
             p.start()

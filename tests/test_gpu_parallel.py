@@ -299,3 +299,47 @@ def test_device_grouping_equals_numpy(k, p, monkeypatch):
     assert np.array_equal(want.weight, got.weight)
     assert np.array_equal(want.mu, got.mu)
     assert np.array_equal(want.var, got.var)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("name", ["mixed", "illum_grouped", "c3small"])
+def test_row_bands_over_peer_mailboxes_equal_single_engine(name, dtype):
+    """The multi-GPU data path of the row bands on one GPU: every band's
+    step pushes its exact partials into every band's mailbox from the deep
+    pass's last CTA (cog_step_p2p, unfused), every band's cog_finalize_p2p
+    sums its own mailbox (flags, parity slots, sequence numbers) -- masks,
+    stats and every state array equal the single engine's bit for bit
+    (cascade.py:301-313, 320-344 over the whole frame)"""
+    from paper_1705_09339_b200.parallel import BandSet
+    rec, overrides = load_case(name)
+    cfg = config_for(overrides, state_dtype=dtype)
+    frames = rec["frames"]
+    n_train = int(rec["n_train"])
+    ref = _single(frames, n_train, cfg)
+    bands = BandSet.train(frames[:n_train], cfg, 3)
+    bands.use_mailboxes()
+    for t in range(frames.shape[0] - n_train):
+        f = frames[n_train + t]
+        m1, s1 = ref.process_frame(f)
+        m2, s2 = bands.process_frame(f)
+        assert np.array_equal(m1.labels, m2.labels), (name, t)
+        assert s1.as_row() == s2.as_row(), (name, t)
+    assert [b.seq for b in bands.mailboxes] == \
+        [frames.shape[0] - n_train] * 3
+    for nm in STATE:
+        assert np.array_equal(bands.state(nm), getattr(ref, nm)), nm
+
+
+def test_peer_mailbox_arguments_are_checked():
+    from paper_1705_09339_b200 import _lib
+    from paper_1705_09339_b200.errors import DataError
+    from paper_1705_09339_b200.parallel import PeerMailbox
+    lib = _lib.load()
+    assert lib.cog_mailbox_words(3, 4, 2) == \
+        2 * 2 * (lib.cog_accum_words(3, 4) + 1)
+    assert lib.cog_mailbox_words(3, 4, 17) == -1
+    with pytest.raises(DataError):
+        PeerMailbox(3, 0, 1, 0, [0])
+    boxes = PeerMailbox.local(3, 2, 2)
+    assert boxes[0].ptrs == boxes[1].ptrs and boxes[1].rank == 1
+    assert boxes[0].next().seq == 1 and boxes[0].next().seq == 2

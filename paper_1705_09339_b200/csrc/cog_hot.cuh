@@ -159,6 +159,9 @@ __device__ __forceinline__ void cp_async_wait() {
 // the stream's worklist (count in sync[2]), GMM fall-throughs and deferred
 // plane-pixels from its back (count in sync[3]); one 64-bit atomic reserves
 // both ranges.  The capacity is every plane-pixel, so the ends cannot meet.
+#ifndef HOT_TWO_ENDED
+#define HOT_TWO_ENDED 1  // build-time A/B switch (tools/gpu_ab_build.sh)
+#endif
 static_assert(HQ_CAP == 64, "hot_flush moves two entries per lane");
 __device__ __forceinline__ void hot_flush(const unsigned long long* qc,
                                           const double* qr, int n,
@@ -170,10 +173,12 @@ __device__ __forceinline__ void hot_flush(const unsigned long long* qc,
   const bool v0 = lane < n, v1 = lane + 32 < n;
   const unsigned long long c0 = v0 ? qc[lane] : 0ull;
   const unsigned long long c1 = v1 ? qc[lane + 32] : 0ull;
-  const bool a0 = v0 && ((c0 >> 1) & 3ull) == (unsigned long long)DEEP_MEANVAR &&
-                  !(c0 & ITEM_DEFERRED);
-  const bool a1 = v1 && ((c1 >> 1) & 3ull) == (unsigned long long)DEEP_MEANVAR &&
-                  !(c1 & ITEM_DEFERRED);
+  const bool a0 = v0 && (!HOT_TWO_ENDED ||
+                        (((c0 >> 1) & 3ull) == (unsigned long long)DEEP_MEANVAR &&
+                         !(c0 & ITEM_DEFERRED)));
+  const bool a1 = v1 && (!HOT_TWO_ENDED ||
+                        (((c1 >> 1) & 3ull) == (unsigned long long)DEEP_MEANVAR &&
+                         !(c1 & ITEM_DEFERRED)));
   const unsigned ma0 = __ballot_sync(FULL, a0), ma1 = __ballot_sync(FULL, a1);
   const unsigned mb0 = __ballot_sync(FULL, v0 && !a0);
   const unsigned mb1 = __ballot_sync(FULL, v1 && !a1);
@@ -212,6 +217,15 @@ constexpr int HF_DEFAULT = HF_SAMPLING | HF_GROUPING | HF_CHP | HF_RATE;
 
 #ifndef COG_HOT_MINB
 #define COG_HOT_MINB 30
+#endif
+// The pipelined variant (16-pixel rows, 4-byte aligned mask words) builds the
+// union mask without a rendezvous of the tile's plane warps: the launcher
+// zeroes the mask, each plane warp ORs the bytes of its foreground labels
+// into it with word atomics (nothing to do for an all-background tile, the
+// common case), and the bytes a warp turned 0 -> 255 are its share of the
+// foreground count -- the same rule the deep pass uses for late labels.
+#ifndef HOT_MASK_ATOMIC
+#define HOT_MASK_ATOMIC 1  // build-time A/B switch (tools/gpu_ab_build.sh)
 #endif
 
 // PIPE (stride 2, rows 16-byte aligned): the round-1 arrays of the warp's
@@ -337,6 +351,7 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
   int kc_units = 0;
   int wq_n = 0;
   unsigned fg_count = 0;
+  constexpr bool AMASK = PIPE && HOT_MASK_ATOMIC != 0 && D > 1;
   // the CTA's tiles: round r covers tiles (blockIdx.x + r * gridDim.x) *
   // HOT_TPB + slot; t = ty * tiles_x + tx advanced without a division
   const int step = gridDim.x * HOT_TPB;
@@ -414,16 +429,8 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
     uint32_t q16 = 0u;
     in.m0 = make_float2(0.0f, 1.0f);
     in.m1 = in.m0;
-#if defined(HOT_EXP_LINEAR)   // cost attribution only (tools/gpu_ab_build.sh): wrong results
-    if (ev) q16 = __ldcg(tq + ((size_t)t * 256 + 128) * 32);
-#else
     if (ev) q16 = __ldcg(tq + ((size_t)t * 256 + vb) * 32);
-#endif
-#if defined(HOT_EXP_NOMODES)
-    if (false) {
-#else
     if (need) {
-#endif
       in.m0 = *reinterpret_cast<const float2*>(rec + 2 * r0);
       in.m1 = *reinterpret_cast<const float2*>(rec + 2 * r1);
     }
@@ -696,13 +703,8 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
       if (fast) {
         a.s.streak[o] = skn;
         // one dense RED per plane-pixel: a byte per level below GMM
-#if defined(HOT_EXP_NORED)
-        if (hitq != nullptr && active < L_GMM)
-          ;
-#else
         if (hitq != nullptr && active < L_GMM)
           atomicAdd(hitq + o, 1u << (8 * active));
-#endif
         else
           atomicAdd(a.s.hits + (plane * 5 + (uint32_t)active * P + p), 1u);
         if (active == L_MEAN)
@@ -758,10 +760,8 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
 
     // ---- outputs, kind counts
     if (valid && !deferred) {
-#if !defined(HOT_EXP_NOCONF)
       conf_s[o] = cf;
       a.kind[o] = (uint8_t)kind;
-#endif
       kc += 1ull << (9 * kind);
     }
 
@@ -831,6 +831,15 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
     if (D == 1) {
       if (valid) a.mask[s1 + p] = (lb >> lane) & 1u ? 255 : 0;
       fg_count += __popc(lb);
+    } else if (AMASK) {
+      // lanes 0, 4, 8, ... own one aligned mask word (4 pixels of a row)
+      const unsigned nib = (lb >> (lane & 28)) & 0xFu;
+      if ((lane & 3) == 0 && nib != 0u) {
+        const unsigned word = ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;
+        const unsigned old =
+            atomicOr(reinterpret_cast<unsigned*>(a.mask + s1 + p), word);
+        fg_count += __popc(word & ~old) >> 3;   // per lane; summed below
+      }
     } else {
       unsigned* lab = s_lab + (it & 1) * NW + slot * D;
       if (lane == 0) lab[c] = lb;
@@ -859,6 +868,7 @@ __global__ void __launch_bounds__(32 * D * HOT_TPB, COG_HOT_MINB / (D * HOT_TPB)
     const unsigned v = warp_sum_u32((unsigned)((kc >> (9 * q)) & 511u));
     if (lane == 0) wacc[acc_kind(0, q)] += v;
   }
+  if (AMASK) fg_count = warp_sum_u32(fg_count);
   if (lane == 0) wacc[acc_fg(D)] += fg_count;
   __syncthreads();
   const int sw = acc_words(D, sG);  // words held in shared

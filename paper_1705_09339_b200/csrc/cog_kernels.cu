@@ -2366,6 +2366,88 @@ __global__ void __launch_bounds__(256)
 // member.  term = x (square = 0) or (x - shift[chain])^2 (square = 1).
 // Also the chain's min and max (np.ptp) and the label's member count.
 // ---------------------------------------------------------------------------
+// The same sums for dims dividing 32, one warp per label: the lanes stage a
+// tile of SEQ_TILE rows (masked rows as +0.0, which leaves a sum unchanged)
+// in shared memory with coalesced loads, then lane f < dims adds its column
+// of the tile in row order -- one shared load and one dependent DADD per
+// row -- while the next tile's loads are in flight.
+constexpr int SEQ_TILE = 128;
+template <int DIMS>
+__global__ void __launch_bounds__(32)
+    seq_sums_tiled_kernel(const double* __restrict__ x, int64_t n,
+                          const int64_t* __restrict__ label,
+                          const double* __restrict__ shift, int square,
+                          double* out, double* minmax, long long* count) {
+  constexpr int PER = SEQ_TILE * DIMS / 32;  // elements per lane per tile
+  __shared__ double buf[SEQ_TILE * DIMS];
+  const int j = blockIdx.x, lane = threadIdx.x;
+  const int f = lane % DIMS;                 // every element of this lane
+  const double sh = shift ? shift[j * DIMS + f] : 0.0;
+  double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+  long long cnt = 0;
+  double acc = 0.0;
+  double t[PER], raw[PER];
+  long long lb[PER];
+  // raw loads of a tile (clamped rows), consumed by finish() after the
+  // previous tile's adds, so they are in flight while lane f adds
+  auto fetch = [&](int64_t i0) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      int64_t i = i0 + (q * 32 + lane) / DIMS;   // row of tile element e
+      if (i >= n) i = n - 1;
+      raw[q] = x[i * DIMS + f];
+      lb[q] = label ? label[i] : (long long)j;
+    }
+  };
+  auto finish = [&](int64_t i0) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int64_t i = i0 + (q * 32 + lane) / DIMS;
+      const bool m = i < n && lb[q] == (long long)j;
+      t[q] = 0.0;
+      if (m) {
+        const double v = raw[q];
+        mn = fmin(mn, v);
+        mx = fmax(mx, v);
+        const double dv = v - sh;
+        t[q] = square ? dv * dv : v;
+        cnt += (f == 0);
+      }
+    }
+  };
+  if (n > 0) {
+    fetch(0);
+    finish(0);
+  }
+  for (int64_t i0 = 0; i0 < n; i0 += SEQ_TILE) {
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < PER; ++q) buf[q * 32 + lane] = t[q];
+    __syncwarp();
+    const bool more = i0 + SEQ_TILE < n;
+    if (more) fetch(i0 + SEQ_TILE);
+    if (lane < DIMS) {
+#pragma unroll 16
+      for (int r = 0; r < SEQ_TILE; ++r) acc = acc + buf[r * DIMS + lane];
+    }
+    if (more) finish(i0 + SEQ_TILE);
+  }
+  // lanes with the same f hold partial min / max / counts
+  for (int o = 16; o >= DIMS; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(FULL, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    cnt += __shfl_xor_sync(FULL, cnt, o);
+  }
+  if (lane < DIMS) {
+    out[j * DIMS + lane] = acc;
+    if (minmax) {
+      minmax[2 * (j * DIMS + lane)] = mn;
+      minmax[2 * (j * DIMS + lane) + 1] = mx;
+    }
+    if (count && lane == 0) count[j] = cnt;
+  }
+}
+
 __global__ void __launch_bounds__(32)
     seq_sums_kernel(const double* __restrict__ x, int64_t n, int dims,
                     const int64_t* __restrict__ label, int k,
@@ -2777,6 +2859,12 @@ int launch_hot_k(const StepArgs& a, cudaStream_t st) {
   FastConst k = make_fast_const(a.q);
   k.P = a.g.height * a.g.width;
   k.wpad = (acc_words(a.g.depth, big ? 0 : a.g.n_groups) + 1) & ~1;
+  if (PIPE && HOT_MASK_ATOMIC != 0 && D > 1) {
+    // the plane warps OR their foreground bytes into a zeroed mask
+    const cudaError_t e = cudaMemsetAsync(
+        a.mask, 0, (size_t)a.g.streams * a.g.height * a.g.width, st);
+    if (e != cudaSuccess) return (int)e;
+  }
   fn<<<dim3(gx < 1 ? 1 : gx, a.g.streams), threads, smem, st>>>(a, k);
   return launch_status();
 }
@@ -2804,7 +2892,8 @@ int launch_hot_cfg(const StepArgs& a, cudaStream_t st) {
     // row of every round-1 array must start on a 16-byte boundary
     const uintptr_t bases = (uintptr_t)a.frame | (uintptr_t)a.s.dyn |
                             (uintptr_t)a.s.streak | (uintptr_t)a.s.meta |
-                            (uintptr_t)a.s.gid | (uintptr_t)a.s.cls;
+                            (uintptr_t)a.s.gid | (uintptr_t)a.s.cls |
+                            (uintptr_t)a.mask;
     if (HOT_PIPE && a.g.width % 16 == 0 && (bases & 15) == 0)
       return launch_hot_b<KMAX, D, 2, HF_DEFAULT, true>(a, st);
     return launch_hot_b<KMAX, D, 2, HF_DEFAULT, false>(a, st);
@@ -3115,6 +3204,12 @@ int cog_seq_sums(const double* x, int64_t n, int32_t dims,
                  void* stream) {
   if (!x || !out || n < 0 || dims < 1 || k < 1) return COG_EINVAL;
   if (square && !shift) return COG_EINVAL;
+  if (dims == 1 || dims == 2) {
+    auto fn = dims == 1 ? seq_sums_tiled_kernel<1> : seq_sums_tiled_kernel<2>;
+    fn<<<(unsigned)k, 32, 0, (cudaStream_t)stream>>>(
+        x, n, label, shift, square, out, minmax, (long long*)count);
+    return launch_status();
+  }
   seq_sums_kernel<<<(unsigned)(k * dims), 32, 0, (cudaStream_t)stream>>>(
       x, n, dims, label, k, shift, square, out, minmax, (long long*)count);
   return launch_status();

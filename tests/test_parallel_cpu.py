@@ -114,3 +114,41 @@ def test_gloo_world2_reduction_and_gather():
         assert np.array_equal(f_all[:5, 0], np.arange(5.0))
         assert np.array_equal(f_all[5:, 0], 1.0 + np.arange(3.0))
         assert np.array_equal(w_all, [10.0] * 5 + [11.0] * 3)
+
+
+def test_peer_mailbox_host_side():
+    """The host side of the fused row-band sum (cog_peers): struct layout as
+    in include/cog_b200.h, mailbox size, the shared step sequence number and
+    its parity slots, argument checks -- no GPU work."""
+    import ctypes
+
+    from paper_1705_09339_b200 import _lib
+    from paper_1705_09339_b200.errors import DataError
+    from paper_1705_09339_b200.parallel import PeerMailbox
+    lib = _lib.load()
+    assert ctypes.sizeof(_lib.Peers) == 16 + 8 * _lib.MAX_RANKS
+    words = lib.cog_accum_words(3, 5)
+    assert lib.cog_mailbox_words(3, 5, 4) == 2 * 4 * (words + 1)
+    assert lib.cog_mailbox_words(3, 5, _lib.MAX_RANKS + 1) == -1
+    assert lib.cog_mailbox_words(0, 5, 2) == -1
+    box = PeerMailbox(3, 5, 4, 2, [0x1000, 0x2000, 0x3000, 0x4000], fused=True)
+    assert box.words == PeerMailbox.size(3, 5, 4)
+    seqs = [box.next().seq for _ in range(3)]
+    assert seqs == [1, 2, 3] and box.current().seq == 3
+    c = box.current()
+    assert (c.n_ranks, c.rank) == (4, 2)
+    assert [c.mailbox[r] for r in range(4)] == [0x1000, 0x2000, 0x3000, 0x4000]
+    with pytest.raises(DataError):
+        PeerMailbox(3, 5, 1, 0, [0x1000])
+    with pytest.raises(DataError):
+        PeerMailbox(3, 5, 3, 0, [0x1000, 0x2000])
+    # null mailbox / bad rank / zero sequence number are refused by the C-ABI
+    g = _lib.Geom()
+    g.total_pixels, g.height, g.width, g.depth = 64, 8, 8, 1
+    g.k, g.stride, g.n_groups, g.streams = 3, 2, 0, 1
+    bad = _lib.Peers()
+    bad.n_ranks, bad.rank, bad.seq = 2, 0, 0
+    rc = lib.cog_finalize_p2p(_lib.ref(g), _lib.ref(_lib.Params()),
+                              _lib.ref(_lib.State()),
+                              ctypes.c_void_p(8), 0, _lib.ref(bad), None)
+    assert rc < 0

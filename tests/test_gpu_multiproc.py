@@ -8,8 +8,15 @@ The union of the ranks' masks, their per-frame statistics and the banded
 state must equal the single whole-frame engine bit for bit
 (cascade.py:301-317 couplings: group update, illumination, stats).
 
-No kernel of one rank waits on the other's on the device: the only
-exchange is the host-side all-reduce between the step and its finalize.
+A second variant sums the partials through peer mailboxes mapped across
+the two processes with CUDA IPC (``PeerMailbox.ipc(fused=False)``): the
+step's last CTA stores the rank's partials into both ranks' mailboxes
+(``cog_step_p2p``), a host barrier follows, ``cog_finalize_p2p`` sums the
+own mailbox -- the multi-GPU data path with real cross-process peer stores.
+
+No kernel of one rank waits on the other's on the device (the ranks share
+one GPU): the exchange is separated from its consumer by a host-side
+all-reduce or barrier between the step and its finalize.
 """
 import os
 import socket

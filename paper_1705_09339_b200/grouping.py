@@ -26,6 +26,10 @@ from .errors import ClusteringError, TrainingError
 
 UNGROUPED = -1
 _POOL_EXACT_BYTES = 1 << 31
+# at scale (build_groups_device) groups above this pooled-sample size take
+# their mean / variance from the GPU's exact integer sums instead of numpy's
+# host pass over (N, d, members) f64 (~0.3 s per group at 720p)
+_POOL_DEVICE_BYTES = 1 << 27
 
 
 @dataclass
@@ -334,7 +338,8 @@ def build_groups_device(features, w_final, values: np.ndarray,
         # 1-D contiguous mean: numpy's own (pairwise) sum on the compacted,
         # order-preserved member weights
         gm.weight[gi] = wf[gid_dev == gi].cpu().numpy().mean()
-        if n_fr * d * int(cnt2[j]) * 8 > _POOL_EXACT_BYTES:
+        if n_fr * d * int(cnt2[j]) * 8 > min(_POOL_EXACT_BYTES,
+                                             _POOL_DEVICE_BYTES):
             big.append(gi)
         else:
             gm.mu[gi], gm.var[gi] = _pooled_stats(values, gm.group_id == gi,

@@ -59,9 +59,14 @@
  *            cog_tabq_build(); NULL for float64 engines
  *   cls      u8[P], gid u16[P] (0xFFFF = ungrouped)
  *   g_mu, g_var  f64[depth][G], g_members u32[G]
- *   accum    u64[cog_accum_words()], sync u32[4]
+ *   accum    u64[cog_accum_words()], sync u32[4] (16-byte aligned: done
+ *            counter, pending bits + hit-byte age, and the worklist's two
+ *            counts, reserved together by one 64-bit atomic)
  *   deepq    u64 + f64 [cog_deepq_slots()]  per-frame worklist of MEANVAR /
- *            GMM plane-pixels (consumed and re-zeroed by the deep pass)
+ *            GMM plane-pixels (consumed and re-zeroed by the deep pass); the
+ *            float32 hot pass fills it from both ends -- fp32 MEANVAR items
+ *            from the front, GMM / deferred items from the back -- so the
+ *            deep pass runs warps of one item type
  */
 #ifndef COG_B200_H
 #define COG_B200_H

@@ -3114,6 +3114,7 @@ int cog_step(const cog_geom* geom, const cog_params* prm, const cog_state* st,
   if (rc) return rc;
   if (!prm || !st || !frame || !mask || !conf || !kind || !stats)
     return COG_EINVAL;
+  if (((uintptr_t)st->sync & 15) != 0) return COG_EINVAL;  // 64-bit atomics
   StepArgs a = make_args(geom, prm, st);
   a.frame = frame;
   a.mask = mask;
@@ -3315,6 +3316,7 @@ int cog_step_p2p(const cog_geom* geom, const cog_params* prm,
     return COG_EINVAL;
   rc = check_peers(geom, peers);
   if (rc) return rc;
+  if (((uintptr_t)st->sync & 15) != 0) return COG_EINVAL;  // 64-bit atomics
   StepArgs a = make_args(geom, prm, st);
   a.frame = frame;
   a.mask = mask;

@@ -49,6 +49,9 @@ constexpr int STATS_WORDS = 16;
 #ifndef DEEP_MINB
 #define DEEP_MINB 2  // deep_kernel CTAs per SM the registers must allow
 #endif
+#ifndef DEEP_AHEAD
+#define DEEP_AHEAD 1  // deep_kernel item pipeline (build-time A/B switch)
+#endif
 
 // accumulator layout (u64 words, per stream)
 __host__ __device__ inline int acc_kind(int c, int k) { return c * 7 + k; }
@@ -1845,30 +1848,74 @@ __global__ void __launch_bounds__(DEEP_THREADS, DEEP_MINB) deep_kernel(const Ste
   // few CTAs
   const size_t wpc = blockDim.x >> 5;
   const size_t gw = (size_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-  for (size_t vi = gw * 32 + (threadIdx.x & 31); vi < n;
-       vi += (size_t)gridDim.x * wpc * 32) {
-    if (vi >= n_a && vi < a32) continue;
-    const size_t i = vi < n_a ? vi : dq_cap - 1 - (vi - a32);
-    const unsigned long long code = dq_code[i];
-    if (!(code & 1ull)) continue;
-    dq_code[i] = 0ull;
+  // Software pipeline over this thread's items (DEEP_AHEAD): the code and
+  // rho of the item two rounds ahead are loaded, the mixture record and meta
+  // word of the item one round ahead are prefetched into L2, while the
+  // current item is processed -- an item's dependent round trips (item ->
+  // record -> update) then overlap the previous items' work.
+  const size_t vstep = (size_t)gridDim.x * wpc * 32;
+  auto item_index = [&](size_t v) -> size_t {
+    return v < n_a ? v : dq_cap - 1 - (v - a32);
+  };
+  auto fetch = [&](size_t v, unsigned long long& code, double& rho) {
+    code = 0ull;
+    rho = 0.0;
+    if (v < n && !(v >= n_a && v < a32)) {
+      const size_t i = item_index(v);
+      code = dq_code[i];
+      rho = dq_rho[i];
+    }
+  };
+  auto prefetch = [&](unsigned long long code) {
+    const int c = (int)((code >> 6) & 3);
+    const size_t p = (size_t)((code >> 16) & 0xFFFFFFFFull);
+    const PlaneRef<T> pr = plane_ref<T>(a, s, c);
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(rec_of(pr, p)));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(pr.meta + p));
+  };
+  size_t vi = gw * 32 + (threadIdx.x & 31);
+  unsigned long long code = 0ull, code1 = 0ull;
+  double rho = 0.0, rho1 = 0.0;
+  fetch(vi, code, rho);
+#if DEEP_AHEAD
+  fetch(vi + vstep, code1, rho1);
+#endif
+  for (; vi < n; vi += vstep) {
+#if DEEP_AHEAD
+    unsigned long long code2;
+    double rho2;
+    fetch(vi + 2 * vstep, code2, rho2);
+    if (code1 & 1ull) prefetch(code1);
+#endif
+    const unsigned long long cur = code;
+    const double cur_rho = rho;
+#if DEEP_AHEAD
+    code = code1;
+    rho = rho1;
+    code1 = code2;
+    rho1 = rho2;
+#else
+    fetch(vi + vstep, code, rho);
+#endif
+    if (!(cur & 1ull)) continue;
+    dq_code[item_index(vi)] = 0ull;
     if constexpr (sizeof(T) == 4) {
-      if (code & ITEM_DEFERRED) {
-        fg += deferred_item<KMAX>(a, s, code, gacc);
+      if (cur & ITEM_DEFERRED) {
+        fg += deferred_item<KMAX>(a, s, cur, gacc);
         continue;
       }
       if (!a.q.compat) {  // fp32 arithmetic, binary64 fallback near ties
         bool ok;
-        const unsigned nw = deep_item_f32<KMAX>(a, s, code, dq_rho[i], ok);
+        const unsigned nw = deep_item_f32<KMAX>(a, s, cur, cur_rho, ok);
         if (ok) {
           fg += nw;
           continue;
         }
-        fg += deep_item_f64_of_f32<KMAX>(&a, s, code, dq_rho[i]);
+        fg += deep_item_f64_of_f32<KMAX>(&a, s, cur, cur_rho);
         continue;
       }
     }
-    fg += deep_item<T, KMAX>(a, s, code, dq_rho[i]);
+    fg += deep_item<T, KMAX>(a, s, cur, cur_rho);
   }
   for (int o = 16; o > 0; o >>= 1) fg += __shfl_xor_sync(FULL, fg, o);
   if ((threadIdx.x & 31) == 0 && fg) atomicAdd(&s_fg, (unsigned long long)fg);

@@ -104,8 +104,7 @@ def test_measure_level_costs_stages_every_level(state_dtype):
     """The level-cost calibration (evaluation.py:180-273) on the CUDA engine:
     each of the six staged frames resolves entirely at its level (the
     calibration raises InternalError otherwise), the costs are positive and
-    normalised by the mixture level, and the cheap levels cost no more than
-    the mixture level on the device either"""
+    normalised by the mixture level"""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -117,4 +116,5 @@ def test_measure_level_costs_stages_every_level(state_dtype):
     assert prof.gmm == 1.0
     assert all(getattr(prof, n) > 0 for n in LEVEL_NAMES)
     assert secs.shape == (6,) and (secs > 0).all()
-    assert prof.skipped <= 1.0 and prof.chp <= 1.0
+    # no ordering of the costs is asserted: at this size a step is a few
+    # tens of microseconds and launch latency dominates every level
